@@ -1,0 +1,475 @@
+"""Benchmark: BASELINE.json's headline on the B200.
+
+Workload (BASELINE configs[1]): 256-bit forward + inverse NTT, n = 2^16, batch
+64 per GPU (weak scaling: every rank runs its own batch of 64; batched NTTs
+shard by transform with no collective).  One step = 64
+forward + 64 inverse transforms = 128 transforms.  metric value = microseconds
+per transform over the whole job (max-over-ranks time / all transforms).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+Other BASELINE configs are parity-test cases; the 256-bit vmul n=2^24 HBM
+figure is reported as an extra "blas" object.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "256-bit NTT µs/transform & BLAS modmul GB/s at 1/2/4/8 B200 vs roofline"
+UNIT = "us/transform"
+BITS, LOGN, BATCH = 256, 16, 64
+N = 1 << LOGN
+K_LIMBS = 8
+WORDS64 = 4  # reference layout: 256-bit = 4 x 64-bit words, MSW first
+# reference algorithmic work = 3k^2 word products per butterfly
+ALG_WMUL_PER_BFLY = 3 * K_LIMBS * K_LIMBS
+L2_BYTES = 126 * 1024 * 1024
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ------------------------------------------------------------ distributed
+def dist_setup(gpus: int):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != gpus:
+        if world == 1 and gpus > 1:
+            raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl" if _cuda_ok() else "gloo")
+        pg = dist
+    return rank, world, local, pg
+
+
+def _cuda_ok():
+    import torch
+    return torch.cuda.is_available()
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def max_over_ranks(pg, value: float) -> float:
+    if pg is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device="cuda" if _cuda_ok() else "cpu")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100", "-i", str(self.dev)],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if self.proc is None or not self.path:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in Path(self.path).read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[2:]))
+            except ValueError:
+                continue
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for _, _, flags in rows for i, f in enumerate(flags) if f.lower() == "active"})
+        loaded = [r[0] for r in rows if r[0] > 0.5 * r[1]] or [r[0] for r in rows]
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+# ------------------------------------------------------------ workload
+def canonical_random(torch, count: int, seed: int):
+    """Uniform canonical residues for the 256-bit prime p ~ 2^252 (< 2^251)."""
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    x = torch.randint(-(1 << 31), 1 << 31, (count, K_LIMBS), dtype=torch.int32, device="cuda", generator=g)
+    x[:, K_LIMBS - 1] &= (1 << 27) - 1
+    return x
+
+
+def flush_l2(torch, buf):
+    buf.add_(1)
+
+
+def peaks():
+    try:
+        return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+    except Exception:
+        return {}
+
+
+def int_peak_wmul_per_s(sm_mhz: float | None):
+    """Integer-pipe roofline: 32 IMAD.WIDE (32x32->64 word products) per clock
+    per SM (measured half-rate, profiles/r01_imad_rate.jsonl) x 148 SMs."""
+    clk = 1965.0
+    return 32 * 148 * clk * 1e6, clk
+
+
+def run_gpu(args, rank, world, local, pg):
+    import torch
+
+    from paper_2501_07535_b200 import device as dev
+    from paper_2501_07535_b200 import kernels as K
+    from paper_2501_07535_b200.params import find_ntt_params
+
+    torch.cuda.set_device(local)
+    prm = find_ntt_params(BITS, N)
+    plan = K.get_plan(BITS, prm)
+    field = plan.field
+    stream = torch.cuda.current_stream()
+
+    x = canonical_random(torch, BATCH * N, 1234 + rank)
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    ws = torch.empty(plan.workspace_bytes(BATCH) // 4, dtype=torch.int32, device="cuda")
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    def step():
+        plan.forward(x, out=y, workspace=ws)
+        plan.inverse(y, out=z, workspace=ws)
+
+    launches_per_step = 2 * len(plan.pass_log_sizes)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    assert torch.equal(z, x), "INTT(NTT(x)) != x in the benchmark workload"
+
+    # ---- device-resident timing (value): per-step events, L2 flushed between steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier(pg)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for s in range(args.steps):
+            flush_l2(torch, flush)
+            ev[s][0].record(stream)
+            step()
+            ev[s][1].record(stream)
+        torch.cuda.synchronize()
+        # forward transform alone (its launches), for the roofline of the NTT passes
+        for s in range(args.steps):
+            flush_l2(torch, flush)
+            fwd_ev[s][0].record(stream)
+            plan.forward(x, out=y, workspace=ws)
+            fwd_ev[s][1].record(stream)
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    local_total_ms = sum(step_ms)
+    barrier(pg)
+    total_ms = max_over_ranks(pg, local_total_ms)
+    transforms = world * args.steps * 2 * BATCH
+    us_per_transform = total_ms * 1e3 / transforms
+
+    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
+
+    # ---- end-to-end through the C ABI with host buffers (reference layout)
+    e2e = run_e2e(args, torch, dev, plan, field, ws, pg, world)
+
+    # ---- BLAS extra: 256-bit vmul n=2^24, HBM GB/s
+    blas = run_blas(args, torch, field, pg)
+
+    return {
+        "us_per_transform": us_per_transform,
+        "ms_per_step": total_ms / args.steps,
+        "fwd_ms": fwd_ms,
+        "pass_log_sizes": plan.pass_log_sizes,
+        "launches_per_step": launches_per_step,
+        "clocks": clocks.summary(),
+        "e2e": e2e,
+        "blas": blas,
+    }
+
+
+def run_e2e(args, torch, dev, plan, field, ws, pg, world):
+    """Host (pinned) reference-layout buffers -> H2D -> layout convert ->
+    NTT -> INTT -> layout convert -> D2H, all inside the timed region."""
+    host_in = torch.empty((BATCH * N, WORDS64), dtype=torch.int64, pin_memory=True)
+    host_out = torch.empty_like(host_in)
+    src = canonical_random(torch, BATCH * N, 99)
+    host_in.copy_(field.to_ref_layout(src, 64, WORDS64).cpu())
+    d_ref = torch.empty((BATCH * N, WORDS64), dtype=torch.int64, device="cuda")
+    d_limbs = torch.empty((BATCH * N, K_LIMBS), dtype=torch.int32, device="cuda")
+    d_y = torch.empty_like(d_limbs)
+    d_out_ref = torch.empty_like(d_ref)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        d_ref.copy_(host_in, non_blocking=True)
+        field.from_ref_layout(d_ref, 64, WORDS64, out=d_limbs)
+        plan.forward(d_limbs, out=d_y, workspace=ws)
+        plan.inverse(d_y, out=d_limbs, workspace=ws)
+        field.to_ref_layout(d_limbs, 64, WORDS64, out=d_out_ref)
+        host_out.copy_(d_out_ref, non_blocking=True)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    assert torch.equal(host_out, host_in), "e2e roundtrip mismatch"
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(pg)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(pg, e0.elapsed_time(e1))
+    nbytes = host_in.numel() * host_in.element_size()
+    return {"value": ms * 1e3 / (world * args.steps * 2 * BATCH), "unit": UNIT,
+            "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
+            "path": "C ABI wm_ref_to_limbs + wm_ntt_forward + wm_ntt_inverse + wm_limbs_to_ref, pinned host buffers"}
+
+
+def run_blas(args, torch, _field, pg):
+    from paper_2501_07535_b200 import device as dev
+    from paper_2501_07535_b200.params import find_ntt_params
+    n = 1 << 24
+    q = find_ntt_params(BITS, 1).p
+    f = dev.Field(BITS, q)
+    a = canonical_random(torch, n, 5)
+    b = canonical_random(torch, n, 6)
+    out = torch.empty_like(a)
+    for _ in range(3):
+        f.vmul(a, b, out=out)
+    torch.cuda.synchronize()
+    reps = 10
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    stream = torch.cuda.current_stream()
+    for s in range(reps):
+        evs[s][0].record(stream)
+        f.vmul(a, b, out=out)
+        evs[s][1].record(stream)
+    torch.cuda.synchronize()
+    ms = statistics.median(x.elapsed_time(y) for x, y in evs)
+    gbs = 3 * 32 * n / (ms * 1e-3) / 1e9
+    hbm = peaks().get("hbm_gbs", 6650.0)
+    return {"op": "vmul", "bits": BITS, "n": n, "ms": ms, "GB_per_s": gbs,
+            "hbm_frac_of_measured": gbs / hbm, "hbm_measured_gbs": hbm,
+            "note": "inputs 1.5 GiB > L2; median of 10"}
+
+
+# ------------------------------------------------------------ CPU baselines
+def _ref_lib():
+    os.environ.setdefault("OMP_STACKSIZE", "64M")
+    path = ROOT / "oracle" / "_ref" / "libref_cpu.so"
+    if not path.exists():
+        return None
+    lib = ctypes.CDLL(str(path))
+    for nm in ("refdrv_ntt65536_256w64", "refdrv_intt65536_256w64"):
+        getattr(lib, nm).argtypes = [ctypes.c_void_p, ctypes.c_int64]
+    return lib
+
+
+def cpu_sample_inputs(count: int):
+    rng = np.random.Generator(np.random.PCG64(7))
+    x = rng.integers(0, 1 << 63, size=(count * N, WORDS64), dtype=np.uint64)
+    x[:, 0] &= np.uint64((1 << 59) - 1)  # MSW-first: top word < 2^59 -> value < 2^251 < p
+    return np.ascontiguousarray(x)
+
+
+def run_cpu_reference(transforms: int):
+    """The reference's own CPU code (emit_c output, oracle/_ref) on all host
+    cores; falls back to the C oracle port when _ref was not built."""
+    cores = len(os.sched_getaffinity(0))
+    lib = _ref_lib()
+    half = max(1, transforms // 2)
+    if lib is not None:
+        x = cpu_sample_inputs(half)
+        y = x.copy()
+        t0 = time.perf_counter()
+        lib.refdrv_ntt65536_256w64(y.ctypes.data, half)
+        lib.refdrv_intt65536_256w64(y.ctypes.data, half)
+        dt = time.perf_counter() - t0
+        assert np.array_equal(x, y), "reference CPU roundtrip mismatch"
+        return {"value": dt * 1e6 / (2 * half), "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"{half} forward + {half} inverse 256-bit n=2^16 transforms, reference emit_c "
+                          f"(64-bit words, gcc -O2) with OpenMP over transforms"}
+    from oracle import bigint
+    from oracle.cbind import OracleField
+    prm = bigint.find_ntt_params(BITS, N)
+    f = OracleField(prm["p"], BITS)
+    x = np.random.Generator(np.random.PCG64(7)).integers(0, 1 << 32, size=(half * N, K_LIMBS), dtype=np.uint64)
+    x = x.astype(np.uint32)
+    x[:, -1] &= (1 << 27) - 1
+    t0 = time.perf_counter()
+    y = f.ntt(x, N, prm["root"])
+    f.ntt(y, N, prm["root_inv"], prm["n_inv"])
+    dt = time.perf_counter() - t0
+    return {"value": dt * 1e6 / (2 * half), "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"{half} forward + {half} inverse transforms, C oracle port (oracle/ntt_oracle.c)"}
+
+
+def reference_arm(args, rank, world, pg):
+    """--impl reference: the reference's CPU implementation of the path."""
+    if rank != 0:
+        return None
+    for _ in range(args.warmup):
+        run_cpu_reference(2)
+    vals = []
+    t_start = time.perf_counter()
+    per_step = args.ref_transforms
+    for _ in range(args.steps):
+        r = run_cpu_reference(per_step)
+        vals.append(r["value"])
+    wall = time.perf_counter() - t_start
+    value = statistics.mean(vals)
+    return {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": wall * 1e3 / args.steps, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32 limbs (256-bit integers)", "data": "synthetic",
+        "config": {"workload": "256-bit forward+inverse NTT n=2^16 (sample of the batch-64 step)",
+                   "bits": BITS, "n": N, "transforms_per_step": 2 * (per_step // 2)},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
+                         "sample": r["sample"]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+# ------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-transforms", type=int, default=32,
+                    help="transforms per reference-arm step (a bounded sample of the 128)")
+    ap.add_argument("--cpu-sample", type=int, default=16)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        log("note: warmup < 3 raised to 3")
+        args.warmup = 3
+
+    rank, world, local, pg = dist_setup(args.gpus)
+    if args.impl == "reference":
+        out = reference_arm(args, rank, world, pg)
+        if rank == 0:
+            print(json.dumps(out))
+        if pg is not None:
+            pg.destroy_process_group()
+        return
+
+    res = run_gpu(args, rank, world, local, pg)
+    if rank != 0:
+        if pg is not None:
+            pg.barrier()
+            pg.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel: the NTT passes (integer pipe)
+    sizes = res["pass_log_sizes"]
+    peak, clk = int_peak_wmul_per_s(res["clocks"].get("sm_mhz"))
+    # full-transform average per launch (passes are near-identical in work)
+    fwd_ms = res["fwd_ms"]  # one forward batch (its pass launches), L2 flushed before
+    bflies_fwd = BATCH * (N // 2) * LOGN
+    achieved = bflies_fwd * ALG_WMUL_PER_BFLY / (fwd_ms * 1e-3)
+    roofline = {
+        "bound": "int", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Twmul/s",
+        "frac": achieved / peak, "traffic": None,
+        "kernel": f"ntt_col_pass/ntt_row_pass ({'+'.join('2^%d' % s for s in sizes)} passes), forward batch 64",
+        "work": f"{ALG_WMUL_PER_BFLY} word products per butterfly (reference 3k^2, SURVEY.md §8(d)) x "
+                f"(n/2) log2 n butterflies",
+        "peak_basis": f"32 IMAD.WIDE/clk/SM x 148 SMs x {clk:.0f} MHz (half-rate IMAD.WIDE measured, "
+                      f"profiles/r01_imad_rate.jsonl)",
+        "ns_per_butterfly_paper_metric": 2 * (fwd_ms * 1e6 / BATCH) / (N * LOGN),
+    }
+    cpu = None
+    if world == 1:
+        try:
+            cpu = run_cpu_reference(args.cpu_sample)
+        except Exception as exc:  # report, do not fail the bench
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "unavailable", "sample": str(exc)}
+    out = {
+        "metric": METRIC,
+        "value": res["us_per_transform"],
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": res["ms_per_step"],
+        "higher_is_better": False,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "u32 limbs (256-bit integers)",
+        "data": "synthetic",
+        "config": {"workload": "256-bit forward+inverse NTT n=2^16 batch 64 per GPU (BASELINE configs[1])",
+                   "bits": BITS, "n": N, "batch_per_gpu": BATCH, "transforms_per_step": 2 * BATCH,
+                   "parallelism": f"batch-sharded x{world}", "l2": "flushed between timed steps (252 MiB write)",
+                   "passes": sizes},
+        "e2e": res["e2e"],
+        "gpu_launches": res["launches_per_step"] * args.steps,
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": res["clocks"],
+        "blas": res["blas"],
+    }
+    print(json.dumps(out))
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,147 @@
+/* widemod_b200 — C ABI of the B200-native multi-word modular arithmetic
+ * library (vadd/vsub/vmul/axpy and radix-2 NTT/INTT over 32..1024-bit prime
+ * fields).
+ *
+ * This is the drop-in boundary for the hot path of the reference package
+ * `widemod` (reference: pkg/src/widemod/).  The reference has no compiled
+ * native code: its device path is CUDA *text* produced by emit.emit_cuda
+ * (emit.py:414-561) with one `extern "C" void {name}_launch(...)` symbol per
+ * (kind, n, bits, word), baked constants, default stream, no error channel
+ * and 32-bit `int` sizes (emit.py:456-484, 545-560; golden
+ * tests/golden/mulmod_16w8.cu:126-137, tests/golden/ntt8_16w8.cu:231-240).
+ * Each entry point below replaces one of those launchers (cited per function)
+ * with a runtime-parameterised version that takes the modulus at run time,
+ * an explicit CUDA stream, 64-bit sizes, and returns a status code.
+ *
+ * Conventions
+ *   - Values are K x 32-bit limbs, least-significant limb first, one element
+ *     after another ("element-contiguous little-endian limbs"); K = limbs of
+ *     the field (wm_field_info).  A value of `bits` interface width occupies
+ *     K = ceil(bits/32) limbs (no power-of-two padding, unlike the reference's
+ *     WordLayout.padded_words, kernels.py:65-71).  wm_ref_to_limbs /
+ *     wm_limbs_to_ref convert from/to the reference's AoS MSW-first word
+ *     layout (kernels.py:418-428).
+ *   - All data pointers are caller-owned DEVICE pointers unless the name says
+ *     _host.  `stream` is a cudaStream_t (NULL = legacy default stream).
+ *     Calls are asynchronous with respect to the host.
+ *   - Inputs must be canonical residues (< modulus), as in the reference
+ *     (oracle.py:7-9); outputs are canonical residues.
+ *   - Every function returns WM_OK (0) or a nonzero status; wm_last_error()
+ *     returns a thread-local message for the last failure on this thread.
+ *   - Plans/fields are immutable after creation and may be shared between
+ *     threads; calls on different streams may run concurrently, except that
+ *     one NTT plan's internal workspace (used when workspace == NULL) is
+ *     serialised by a mutex.
+ */
+#ifndef WIDEMOD_B200_H
+#define WIDEMOD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WM_ABI_VERSION 1
+
+#define WM_OK 0
+#define WM_EINVAL 1        /* bad argument (reference: ValueError family) */
+#define WM_ECUDA 2         /* CUDA runtime failure */
+#define WM_EUNSUPPORTED 3  /* limb count / size not built into this library */
+#define WM_ELENGTH 4       /* length mismatch (reference: LengthMismatch) */
+
+typedef struct wm_field wm_field;
+typedef struct wm_ntt_plan wm_ntt_plan;
+
+int wm_abi_version(void);
+const char *wm_last_error(void);
+
+/* Limb count the library uses for an interface width (ceil(bits/32)), or -1
+ * if that width is not built in.  Mirrors WordLayout(bits, 32).words
+ * (kernels.py:61-63). */
+int wm_limbs_for_bits(int bits);
+
+/* Writes the built-in limb counts for the BLAS kernels (ntt=0) or the NTT
+ * kernels (ntt=1) to out[0..cap), returns how many there are. */
+int wm_supported_limbs(int ntt, int *out, int cap);
+
+/* ---------------------------------------------------------------- fields
+ * A field is a modulus q for an interface width `bits` together with the
+ * device-side reduction constants.  Replaces the constants the reference
+ * bakes into generated code (kernels._param_vars kernels.py:168-181,
+ * oracle.compute_barrett oracle.py:109-134).  Requires
+ * 2^(bits-5) < q < 2^(bits-4) (the reference's Barrett range, oracle.py:124-128)
+ * or more generally 1 < q < 2^(32K-4) with bit length > 32K-36.
+ * q is given as q_limbs little-endian 32-bit limbs (host memory). */
+int wm_field_create(int bits, const uint32_t *q_host, int q_limbs, wm_field **out);
+int wm_field_destroy(wm_field *f);
+int wm_field_info(const wm_field *f, int *bits, int *limbs, int *norm_shift);
+
+/* ---------------------------------------------------------------- BLAS
+ * Replace `{kind}{n}_{bits}w{word}_launch(const w *a, const w *b, w *out,
+ * int n_elems)` (emit.py:456-484) for kind in vadd/vsub/vmul: out[i] =
+ * a[i] (+,-,*) b[i] mod q for i < n.  out may alias a or b.
+ * Semantics: reference build_vector kernels.py:215-256. */
+int wm_vadd(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out,
+            int64_t n, void *stream);
+int wm_vsub(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out,
+            int64_t n, void *stream);
+int wm_vmul(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out,
+            int64_t n, void *stream);
+/* Replaces the axpy launcher `(const w *a, const w *x, const w *y, w *out,
+ * int n_elems)` whose scalar `a` is an un-indexed device pointer
+ * (emit.py:463-472, vector_args=[False,True,True] kernels.py:228-230):
+ * out[i] = a*x[i] + y[i] mod q.  Here the scalar is passed by value from
+ * HOST memory (K limbs), so no device round trip is needed. */
+int wm_axpy(const wm_field *f, const uint32_t *a_host, const uint32_t *x, const uint32_t *y,
+            uint32_t *out, int64_t n, void *stream);
+
+/* ---------------------------------------------------------------- NTT
+ * A plan for length-n (power of two, 2 <= n <= 2^30) cyclic transforms over
+ * the field's prime p = q with root of exact order n (reference NttParams,
+ * oracle.py:74-82; find_ntt_params oracle.py:186-239).  root, root_inv and
+ * n_inv are canonical residues, K limbs each (host memory).  Twiddle tables
+ * are generated on the device at plan creation. */
+int wm_ntt_plan_create(const wm_field *f, int64_t n, const uint32_t *root_host,
+                       const uint32_t *root_inv_host, const uint32_t *n_inv_host,
+                       wm_ntt_plan **out);
+int wm_ntt_plan_destroy(wm_ntt_plan *p);
+/* Number of passes and per-pass sub-transform sizes (log2) of the plan. */
+int wm_ntt_plan_info(const wm_ntt_plan *p, int *passes, int *log_sizes, int cap);
+
+/* Bytes of device workspace a call with this batch needs (0 for one-pass
+ * plans).  Pass workspace=NULL to let the plan use (and grow) its own. */
+int64_t wm_ntt_workspace_bytes(const wm_ntt_plan *p, int64_t batch);
+
+/* Replace `ntt{n}_{bits}w{word}_launch(const w *in, w *x, int batch)` and the
+ * intt equivalent (emit.py:545-560): for each of `batch` contiguous
+ * transforms, out = NTT(in) with y[k] = sum_j x[j] root^(jk) mod p (forward)
+ * or out = n^-1 sum_j x[j] root^(-jk) (inverse), natural order in and out —
+ * bit-identical to reference run_ntt (kernels.py:483-499) and ntt_reference
+ * (oracle.py:262-282).  in may equal out. */
+int wm_ntt_forward(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int64_t batch,
+                   void *workspace, void *stream);
+int wm_ntt_inverse(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int64_t batch,
+                   void *workspace, void *stream);
+
+/* Copies twiddle powers root^e (inverse: root_inv^e) for e in [0, count) into
+ * out (device, count*K limbs): the reference twiddle_table (kernels.py:259-267)
+ * is the first n/2 of them. */
+int wm_ntt_twiddles(const wm_ntt_plan *p, int inverse, int64_t count, uint32_t *out,
+                    void *stream);
+
+/* ---------------------------------------------------------------- layout
+ * Reference layout: AoS, `ref_words` words of `word_bits` (32 or 64) per
+ * element, most-significant word first (kernels.to_words kernels.py:418-421;
+ * emit_cuda element pointers `a + i * per_arg`, emit.py:466-470).  Words above
+ * the K limbs must be zero on input and are written as zero on output. */
+int wm_ref_to_limbs(int word_bits, int ref_words, int limbs, const void *ref, uint32_t *out,
+                    int64_t n, void *stream);
+int wm_limbs_to_ref(int word_bits, int ref_words, int limbs, const uint32_t *in, void *ref,
+                    int64_t n, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WIDEMOD_B200_H */

@@ -1,0 +1,99 @@
+"""TEST INFRASTRUCTURE ONLY — build oracle/_ref/libref_cpu.so: the reference's
+own CPU code for the hot path.
+
+The reference (/root/reference/pkg/src/widemod) has no compiled native code;
+its fastest CPU path is the portable C its emitter writes
+(emit.emit_c, emit.py:281-411: straight-line limb code on 64-bit words with
+unsigned __int128 products, baked q/mu, and for transforms the run_ntt loop
+structure with baked twiddle and bit-reversal tables).  This script imports
+the reference package, emits that C for the benchmark kernels into
+oracle/_ref/ (git-ignored; it travels to the GPU box with the snapshot), adds
+a thin OpenMP driver of our own around each emitted translation unit, and
+compiles everything with gcc -O2.  Only runs where /root/reference exists.
+"""
+
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+HERE = Path(__file__).resolve().parent
+OUT = HERE / "_ref"
+REF_SRC = Path("/root/reference/pkg/src")
+
+# (kind, bits, word, size): the bench workload's transforms and the BLAS sweep
+NTT_KERNELS = [("ntt", 256, 64, 1 << 16), ("intt", 256, 64, 1 << 16)]
+BLAS_KERNELS = [(k, b, 64, 1) for b in (128, 256, 384, 768) for k in ("vadd", "vmul", "axpy")]
+
+
+def _driver_ntt(name: str, n: int, per_arg: int) -> str:
+    return f"""
+#include <stdint.h>
+void refdrv_{name}(uint64_t *x, int64_t batch) {{
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int64_t b = 0; b < batch; ++b)
+    {name}_transform((w64 (*)[{per_arg}])(x + b * (int64_t){n} * {per_arg}));
+}}
+"""
+
+
+def _driver_vec(name: str, kind: str, per_arg: int) -> str:
+    if kind == "axpy":
+        return f"""
+#include <stdint.h>
+void refdrv_{name}(const uint64_t *a, const uint64_t *x, const uint64_t *y, uint64_t *out, int64_t n) {{
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i)
+    {name}(a, x + i * {per_arg}, y + i * {per_arg}, out + i * {per_arg});
+}}
+"""
+    return f"""
+#include <stdint.h>
+void refdrv_{name}(const uint64_t *x, const uint64_t *y, uint64_t *out, int64_t n) {{
+#pragma omp parallel for schedule(static)
+  for (int64_t i = 0; i < n; ++i)
+    {name}(x + i * {per_arg}, y + i * {per_arg}, out + i * {per_arg});
+}}
+"""
+
+
+def main() -> int:
+    if not REF_SRC.exists():
+        print("gen_ref: /root/reference not present; skipping (prebuilt _ref is used if shipped)")
+        return 0
+    sys.path.insert(0, str(REF_SRC))
+    from widemod.emit import emit_c  # reference emitter
+    from widemod.kernels import generate_kernel, make_spec
+
+    OUT.mkdir(exist_ok=True)
+    units = []
+    for kind, bits, word, size in NTT_KERNELS + BLAS_KERNELS:
+        prog = generate_kernel(make_spec(kind, bits, word, size=size))
+        name = prog.name
+        per_arg = prog.attributes["padded_bits"] // word
+        src = emit_c(prog)
+        body = OUT / f"{name}.emitted.c"
+        body.write_text(src)
+        drv = _driver_ntt(name, size, per_arg) if kind in ("ntt", "intt") else _driver_vec(name, kind, per_arg)
+        unit = OUT / f"{name}.unit.c"
+        unit.write_text(f'#include "{body.name}"\n' + drv)
+        units.append(unit)
+        print(f"gen_ref: emitted {name} ({len(src) // 1024} KiB)", flush=True)
+    objs = []
+    for u in units:
+        o = u.with_suffix(".o")
+        subprocess.run(["gcc", "-O2", "-fPIC", "-fopenmp", "-c", str(u), "-o", str(o)], check=True)
+        objs.append(str(o))
+    lib = OUT / "libref_cpu.so"
+    subprocess.run(["gcc", "-shared", "-fopenmp", "-o", str(lib), *objs], check=True)
+    for o in objs:
+        os.remove(o)
+    (OUT / "MANIFEST").write_text("\n".join(f"{k} {b} {w} {s}" for k, b, w, s in NTT_KERNELS + BLAS_KERNELS) + "\n")
+    print(f"gen_ref: built {lib}")
+    return 0
+
+
+if __name__ == "__main__":
+    raise SystemExit(main())

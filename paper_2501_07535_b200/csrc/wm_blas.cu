@@ -1,0 +1,373 @@
+// Element-wise modular BLAS (vadd/vsub/vmul/axpy), field setup, layout
+// converters and the library's error channel.
+//
+// Reference semantics: build_vector (kernels.py:215-256) over _emit_addmod /
+// _emit_submod / _emit_mulmod (kernels.py:122-153); reference GPU form: the
+// one-thread-per-element kernels of emit_cuda (emit.py:454-484).
+//
+// B200 design: one element per thread per iteration of a grid-stride loop over
+// element-contiguous little-endian limbs; every operand is moved with the
+// widest legal vector access (256-bit LDG/STG for 8 | K), so a warp moves a
+// contiguous 32*4K-byte span per operand.  The modulus and its reduction
+// constants are a __grid_constant__ kernel parameter (uniform, constant-bank
+// resident) rather than baked constants, so one binary serves every modulus
+// of a width (the reference bakes q/mu per kernel, kernels.py:168-181).
+#include <algorithm>
+#include <cstdio>
+
+#include "wm_internal.cuh"
+#include "wm_io.cuh"
+
+namespace wm {
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int fail(int code, const std::string &msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char *what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return WM_ECUDA;
+}
+
+bool blas_supports(int K) {
+  switch (K) {
+#define WM_CASE(k) case k:
+    WM_BLAS_KS(WM_CASE)
+#undef WM_CASE
+    return true;
+    default:
+      return false;
+  }
+}
+
+bool ntt_supports(int K) {
+  switch (K) {
+#define WM_CASE(k) case k:
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    return true;
+    default:
+      return false;
+  }
+}
+
+// ------------------------------------------------------------------ host bignum
+int big_bitlen(const Big &a) {
+  for (int j = (int)a.size() - 1; j >= 0; --j)
+    if (a[j]) return 32 * j + (32 - __builtin_clz(a[j]));
+  return 0;
+}
+
+Big big_resize(const Big &a, int limbs) {
+  Big r(limbs, 0u);
+  for (int j = 0; j < limbs && j < (int)a.size(); ++j) r[j] = a[j];
+  return r;
+}
+
+Big big_shl(const Big &a, int s, int limbs) {
+  Big r(limbs, 0u);
+  int ls = s / 32, bs = s % 32;
+  for (int j = limbs - 1; j >= 0; --j) {
+    int src = j - ls;
+    uint64_t v = 0;
+    if (src >= 0 && src < (int)a.size()) v = (uint64_t)a[src] << bs;
+    if (bs && src - 1 >= 0 && src - 1 < (int)a.size()) v |= (uint64_t)a[src - 1] >> (32 - bs);
+    r[j] = (uint32_t)v;
+  }
+  return r;
+}
+
+bool big_ge(const Big &a, const Big &b) {
+  for (int j = (int)a.size() - 1; j >= 0; --j) {
+    if (a[j] != b[j]) return a[j] > b[j];
+  }
+  return true;
+}
+
+void big_sub_inplace(Big &a, const Big &b) {
+  uint64_t br = 0;
+  for (size_t j = 0; j < a.size(); ++j) {
+    uint64_t d = (uint64_t)a[j] - b[j] - br;
+    a[j] = (uint32_t)d;
+    br = (d >> 63) & 1;
+  }
+}
+
+Big big_pow2_div(int e, const Big &d, int limbs) {
+  // remainder lives in d.size()+1 limbs; quotient bits produced MSB first
+  const int L = (int)d.size() + 1;
+  Big dd = big_resize(d, L);
+  Big rem(L, 0u);
+  Big quo(limbs, 0u);
+  for (int bit = e; bit >= 0; --bit) {
+    // rem = 2*rem + (bit == e ? 1 : 0)
+    uint32_t carry = (bit == e) ? 1u : 0u;
+    for (int j = 0; j < L; ++j) {
+      uint32_t nc = rem[j] >> 31;
+      rem[j] = (rem[j] << 1) | carry;
+      carry = nc;
+    }
+    if (big_ge(rem, dd)) {
+      big_sub_inplace(rem, dd);
+      if (bit / 32 < limbs) quo[bit / 32] |= 1u << (bit % 32);
+    }
+  }
+  return quo;
+}
+
+// ------------------------------------------------------------------ field
+template <int K>
+FieldConst<K> field_const(const wm_field *f) {
+  FieldConst<K> c;
+  for (int j = 0; j < K; ++j) {
+    c.q[j] = f->q[j];
+    c.qn[j] = f->qn[j];
+    c.qn2[j] = f->qn2[j];
+    c.nqn[j] = f->nqn[j];
+    c.mu8[j] = f->mu8[j];
+  }
+  c.s = (uint32_t)f->s;
+  return c;
+}
+
+// ------------------------------------------------------------------ kernels
+enum BlasOp { OP_VADD = 0, OP_VSUB = 1, OP_VMUL = 2, OP_AXPY = 3 };
+
+template <int K>
+struct BlasArgs {
+  FieldConst<K> F;
+  uint32_t scal[K];  // axpy scalar, pre-shifted by F.s
+};
+
+template <int K, int OP>
+__global__ void __launch_bounds__(256) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
+                                                   int64_t n, const __grid_constant__ BlasArgs<K> args) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint32_t x[K], y[K], r[K];
+    load_elem<K>(x, a, i);
+    load_elem<K>(y, b, i);
+    if constexpr (OP == OP_VADD) {
+      add_mod<K>(r, x, y, args.F.q);
+    } else if constexpr (OP == OP_VSUB) {
+      sub_mod<K>(r, x, y, args.F.q);
+    } else if constexpr (OP == OP_VMUL) {
+      mul_barrett<K>(r, x, y, args.F);
+    } else {
+      uint32_t t[K];
+      mul_barrett_pre<K>(t, args.scal, x, args.F);
+      add_mod<K>(r, t, y, args.F.q);
+    }
+    store_elem<K>(out, i, r);
+  }
+}
+
+template <int K, int OP>
+static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out,
+                       int64_t n, const uint32_t *scal_host, cudaStream_t st) {
+  static int blocks_per_sm = -1;
+  static int sm_count = 0;
+  if (blocks_per_sm < 0) {
+    int dev;
+    WM_CUDA_TRY(cudaGetDevice(&dev));
+    WM_CUDA_TRY(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
+    int nb = 0;
+    WM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, blas_kernel<K, OP>, 256, 0));
+    blocks_per_sm = std::max(1, nb);
+  }
+  BlasArgs<K> args;
+  args.F = field_const<K>(f);
+  for (int j = 0; j < K; ++j) args.scal[j] = 0;
+  if (scal_host) {
+    Big sh = big_shl(Big(scal_host, scal_host + K), f->s, K);
+    for (int j = 0; j < K; ++j) args.scal[j] = sh[j];
+  }
+  int64_t want = (n + 255) / 256;
+  int64_t cap = (int64_t)sm_count * blocks_per_sm * 4;  // a few waves' worth of resident CTAs
+  int grid = (int)std::max<int64_t>(1, std::min(want, cap));
+  blas_kernel<K, OP><<<grid, 256, 0, st>>>(a, b, out, n, args);
+  WM_LAUNCH_CHECK("blas_kernel launch");
+  return WM_OK;
+}
+
+static int blas_dispatch(int op, const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out,
+                         int64_t n, const uint32_t *scal_host, void *stream) {
+  if (!f) return fail(WM_EINVAL, "null field");
+  if (n < 0) return fail(WM_EINVAL, "negative length");
+  if (n == 0) return WM_OK;
+  if (!a || !b || !out) return fail(WM_EINVAL, "null data pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (f->K) {
+#define WM_CASE(k)                                                                     \
+  case k:                                                                              \
+    switch (op) {                                                                      \
+      case OP_VADD: return launch_blas<k, OP_VADD>(f, a, b, out, n, nullptr, st);      \
+      case OP_VSUB: return launch_blas<k, OP_VSUB>(f, a, b, out, n, nullptr, st);      \
+      case OP_VMUL: return launch_blas<k, OP_VMUL>(f, a, b, out, n, nullptr, st);      \
+      default: return launch_blas<k, OP_AXPY>(f, a, b, out, n, scal_host, st);         \
+    }
+    WM_BLAS_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      return fail(WM_EUNSUPPORTED, "limb count not built into the BLAS kernels");
+  }
+}
+
+// ------------------------------------------------------------------ layout
+__global__ void ref_to_limbs_kernel(int word_bits, int R, int K, const void *ref, uint32_t *out, int64_t total) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    int64_t i = idx / K;
+    int j = (int)(idx - i * K);
+    uint32_t v;
+    if (word_bits == 64) {
+      int w = j / 2;
+      uint64_t word = (w < R) ? static_cast<const uint64_t *>(ref)[i * R + (R - 1 - w)] : 0ull;
+      v = (uint32_t)(word >> (32 * (j & 1)));
+    } else {
+      v = (j < R) ? static_cast<const uint32_t *>(ref)[i * R + (R - 1 - j)] : 0u;
+    }
+    out[idx] = v;
+  }
+}
+
+__global__ void limbs_to_ref_kernel(int word_bits, int R, int K, const uint32_t *in, void *ref, int64_t total) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += stride) {
+    int64_t i = idx / R;
+    int w = (int)(idx - i * R);  // 0 = most significant word
+    int lw = R - 1 - w;          // little-endian word index
+    if (word_bits == 64) {
+      uint32_t lo = (2 * lw < K) ? in[i * K + 2 * lw] : 0u;
+      uint32_t hi = (2 * lw + 1 < K) ? in[i * K + 2 * lw + 1] : 0u;
+      static_cast<uint64_t *>(ref)[idx] = ((uint64_t)hi << 32) | lo;
+    } else {
+      static_cast<uint32_t *>(ref)[idx] = (lw < K) ? in[i * K + lw] : 0u;
+    }
+  }
+}
+
+}  // namespace wm
+
+using namespace wm;
+
+extern "C" {
+
+int wm_abi_version(void) { return WM_ABI_VERSION; }
+
+const char *wm_last_error(void) { return g_last_error.c_str(); }
+
+int wm_limbs_for_bits(int bits) {
+  if (bits < 1) return -1;
+  int K = (bits + 31) / 32;
+  return blas_supports(K) ? K : -1;
+}
+
+int wm_supported_limbs(int ntt, int *out, int cap) {
+  int ks[64];
+  int m = 0;
+  if (ntt) {
+#define WM_CASE(k) ks[m++] = k;
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+  } else {
+#define WM_CASE(k) ks[m++] = k;
+    WM_BLAS_KS(WM_CASE)
+#undef WM_CASE
+  }
+  for (int i = 0; i < m && i < cap; ++i) out[i] = ks[i];
+  return m;
+}
+
+int wm_field_create(int bits, const uint32_t *q_host, int q_limbs, wm_field **out) {
+  if (!out) return fail(WM_EINVAL, "null output pointer");
+  *out = nullptr;
+  if (bits < 8) return fail(WM_EINVAL, "width must be at least 8 bits");
+  if (!q_host || q_limbs < 1) return fail(WM_EINVAL, "null modulus");
+  int K = (bits + 31) / 32;
+  if (!blas_supports(K)) return fail(WM_EUNSUPPORTED, "width " + std::to_string(bits) + " (" +
+                                                          std::to_string(K) + " limbs) not built in");
+  Big q(q_host, q_host + q_limbs);
+  for (int j = K; j < q_limbs; ++j)
+    if (q[j]) return fail(WM_EINVAL, "modulus wider than the field width");
+  q = big_resize(q, K);
+  int qb = big_bitlen(q);
+  const int M = 32 * K - 4;
+  if (qb < 2) return fail(WM_EINVAL, "modulus must exceed 1");
+  if (qb > M) return fail(WM_EINVAL, "modulus must be below 2^(32K-4)");
+  if (M - qb > 31) return fail(WM_EINVAL, "modulus too small for the field width (normalisation shift > 31)");
+  wm_field *f = new wm_field();
+  f->bits = bits;
+  f->K = K;
+  f->s = M - qb;
+  f->q = q;
+  f->qn = big_shl(q, f->s, K);
+  f->qn2 = big_shl(f->qn, 1, K);
+  Big zero(K, 0u);
+  f->nqn = zero;
+  big_sub_inplace(f->nqn, f->qn);  // 2^(32K) - qn (mod 2^(32K))
+  Big mu = big_pow2_div(2 * M, f->qn, K);
+  f->mu8 = big_shl(mu, 3, K);
+  *out = f;
+  return WM_OK;
+}
+
+int wm_field_destroy(wm_field *f) {
+  delete f;
+  return WM_OK;
+}
+
+int wm_field_info(const wm_field *f, int *bits, int *limbs, int *norm_shift) {
+  if (!f) return fail(WM_EINVAL, "null field");
+  if (bits) *bits = f->bits;
+  if (limbs) *limbs = f->K;
+  if (norm_shift) *norm_shift = f->s;
+  return WM_OK;
+}
+
+int wm_vadd(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, void *stream) {
+  return blas_dispatch(OP_VADD, f, a, b, out, n, nullptr, stream);
+}
+int wm_vsub(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, void *stream) {
+  return blas_dispatch(OP_VSUB, f, a, b, out, n, nullptr, stream);
+}
+int wm_vmul(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, void *stream) {
+  return blas_dispatch(OP_VMUL, f, a, b, out, n, nullptr, stream);
+}
+int wm_axpy(const wm_field *f, const uint32_t *a_host, const uint32_t *x, const uint32_t *y, uint32_t *out,
+            int64_t n, void *stream) {
+  if (!a_host) return fail(WM_EINVAL, "null scalar");
+  return blas_dispatch(OP_AXPY, f, x, y, out, n, a_host, stream);
+}
+
+int wm_ref_to_limbs(int word_bits, int ref_words, int limbs, const void *ref, uint32_t *out, int64_t n,
+                    void *stream) {
+  if (word_bits != 32 && word_bits != 64) return fail(WM_EINVAL, "word_bits must be 32 or 64");
+  if (ref_words < 1 || limbs < 1 || n < 0) return fail(WM_EINVAL, "bad shape");
+  if (n == 0) return WM_OK;
+  int64_t total = n * limbs;
+  int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+  ref_to_limbs_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(word_bits, ref_words, limbs, ref, out, total);
+  WM_LAUNCH_CHECK("ref_to_limbs launch");
+  return WM_OK;
+}
+
+int wm_limbs_to_ref(int word_bits, int ref_words, int limbs, const uint32_t *in, void *ref, int64_t n,
+                    void *stream) {
+  if (word_bits != 32 && word_bits != 64) return fail(WM_EINVAL, "word_bits must be 32 or 64");
+  if (ref_words < 1 || limbs < 1 || n < 0) return fail(WM_EINVAL, "bad shape");
+  if (n == 0) return WM_OK;
+  int64_t total = n * ref_words;
+  int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 32);
+  limbs_to_ref_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(word_bits, ref_words, limbs, in, ref, total);
+  WM_LAUNCH_CHECK("limbs_to_ref launch");
+  return WM_OK;
+}
+
+}  // extern "C"

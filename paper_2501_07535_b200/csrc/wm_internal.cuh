@@ -1,0 +1,93 @@
+// Host-side internals shared by the library's translation units: error
+// channel, small host bignum helpers for parameter setup, the field and plan
+// objects, and the limb-count dispatch tables.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/widemod_b200.h"
+#include "wm_limb.cuh"
+
+namespace wm {
+
+// ------------------------------------------------------------------ errors
+void set_error(const std::string &msg);
+int fail(int code, const std::string &msg);
+int cuda_fail(cudaError_t e, const char *what);
+
+#define WM_CUDA_TRY(expr)                                  \
+  do {                                                     \
+    cudaError_t _e = (expr);                               \
+    if (_e != cudaSuccess) return ::wm::cuda_fail(_e, #expr); \
+  } while (0)
+
+// After a kernel launch: report launch-configuration errors synchronously.
+#define WM_LAUNCH_CHECK(what)                              \
+  do {                                                     \
+    cudaError_t _e = cudaGetLastError();                   \
+    if (_e != cudaSuccess) return ::wm::cuda_fail(_e, what); \
+  } while (0)
+
+// ------------------------------------------------------------------ limb sets
+// Limb counts compiled into the library.  K = ceil(bits/32).
+#define WM_BLAS_KS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(16) X(24) X(32)
+#define WM_NTT_KS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(12) X(16) X(24)
+
+bool blas_supports(int K);
+bool ntt_supports(int K);
+
+// ------------------------------------------------------------------ host bignum
+using Big = std::vector<uint32_t>;  // little-endian limbs, fixed length
+int big_bitlen(const Big &a);
+Big big_shl(const Big &a, int s, int limbs);          // (a << s) truncated to limbs
+bool big_ge(const Big &a, const Big &b);               // same length
+void big_sub_inplace(Big &a, const Big &b);            // a -= b, same length, a >= b
+Big big_resize(const Big &a, int limbs);
+// floor(2^e / d) truncated to `limbs` limbs (binary long division).
+Big big_pow2_div(int e, const Big &d, int limbs);
+
+// ------------------------------------------------------------------ objects
+}  // namespace wm
+
+struct wm_field {
+  int bits = 0;
+  int K = 0;
+  int s = 0;
+  wm::Big q, qn, qn2, nqn, mu8;  // K limbs each
+};
+
+struct wm_ntt_pass {
+  bool column = false;  // column pass (strided lines) vs row pass (contiguous lines)
+  int logL = 0;         // sub-transform size
+  int G = 1;            // lines per CTA
+  // column pass: line (o, i); read pos = o*RO + t*RT + i; write pos = o*WO + k*WK + i
+  // row pass:    line r;      read pos = r*L + t;         write pos = r*WO + k*WK
+  int64_t lines_inner = 1, lines_outer = 1;
+  int64_t RO = 0, RT = 0, WO = 0, WK = 0;
+  // twiddle on output: e = ((i >> SH) * (o*C1 + k*C2) * C3) mod n; C3 == 0: none
+  int SH = 0;
+  int64_t C1 = 0, C2 = 0, C3 = 0;
+  bool scaled_table = false;  // inverse: use the n^-1-scaled table for this pass
+  bool scale_out = false;     // inverse one-pass plans: multiply outputs by n^-1
+  int src = 0, dst = 0;       // 0 = user in/out, 1 = workspace (see plan creation)
+};
+
+struct wm_ntt_plan {
+  const wm_field *field = nullptr;
+  int K = 0;
+  int64_t n = 0;
+  int logn = 0;
+  std::vector<wm_ntt_pass> passes;
+  // device tables: n entries of (w, w') pairs (2K words each)
+  uint32_t *tw_fwd = nullptr, *tw_inv = nullptr, *tw_inv_scaled = nullptr;
+  wm::Big ninv, ninv_sh, np;  // n^-1, floor(n^-1 * 2^32K / p), 2^32K - p
+  // internal workspace (used when the caller passes none)
+  std::mutex ws_mu;
+  void *ws = nullptr;
+  int64_t ws_bytes = 0;
+};

@@ -1,0 +1,270 @@
+// Multi-word (K x 32-bit limb) modular arithmetic core for sm_100a.
+//
+// This is the B200 counterpart of the reference's recursive type rewriting
+// (reference pkg/src/widemod/rewrite.py: mw_add 122-137, mw_sub 140-171,
+// mw_lt 174-192, mw_mul 217-253, mw_shr 256-281, lower_mod_after_add 311-321,
+// lower_modsub 324-330, lower_modmul_barrett 333-351).  Where the reference
+// lowers a wide IR value into machine words at code-generation time, here the
+// limb loops are fully unrolled per limb count K by templates.
+//
+// Layout of a value: uint32_t v[K], least-significant limb first.
+//
+// Instruction-selection notes (measured on B200, profiles/r01_*.jsonl):
+//   * IMAD (32-bit lo) issues at 64/clk/SM, IMAD.HI and IMAD.WIDE at 32/clk/SM.
+//   * PTX mad.lo.cc/madc.hi.cc pairs lower to IMAD + IMAD.HI + 2x IADD3, i.e.
+//     three FMA-pipe slots per 32x32->64 product.  Writing products as
+//     (uint64_t)a*b lets ptxas emit one IMAD.WIDE (two slots) and route the
+//     carry adds to the ALU pipe, so every multiplier below uses that form.
+//   * add/sub carry chains use PTX add.cc/addc (lowered to IADD3 with carry
+//     predicates on the ALU pipe).  They are asm volatile so NVVM never
+//     reorders a chain; ptxas tracks the carry as a predicate register.
+#pragma once
+#include <cstdint>
+
+#define WM_DEV __device__ __forceinline__
+
+namespace wm {
+
+// ------------------------------------------------------------------ add/sub
+// r = a + b (mod 2^(32K)); returns the carry out (0 or 1).
+template <int K>
+WM_DEV uint32_t add_n(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  if (K == 1) {
+    uint32_t c;
+    asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(r[0]) : "r"(a[0]), "r"(b[0]));
+    asm volatile("addc.u32 %0, 0, 0;" : "=r"(c));
+    return c;
+  }
+  asm volatile("add.cc.u32 %0, %1, %2;" : "=r"(r[0]) : "r"(a[0]), "r"(b[0]));
+#pragma unroll
+  for (int j = 1; j < K; ++j)
+    asm volatile("addc.cc.u32 %0, %1, %2;" : "=r"(r[j]) : "r"(a[j]), "r"(b[j]));
+  uint32_t c;
+  asm volatile("addc.u32 %0, 0, 0;" : "=r"(c));
+  return c;
+}
+
+// r = a - b (mod 2^(32K)); returns 0xffffffff if a < b (a borrow), else 0.
+template <int K>
+WM_DEV uint32_t sub_n(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  asm volatile("sub.cc.u32 %0, %1, %2;" : "=r"(r[0]) : "r"(a[0]), "r"(b[0]));
+#pragma unroll
+  for (int j = 1; j < K; ++j)
+    asm volatile("subc.cc.u32 %0, %1, %2;" : "=r"(r[j]) : "r"(a[j]), "r"(b[j]));
+  uint32_t br;
+  asm volatile("subc.u32 %0, 0, 0;" : "=r"(br));
+  return br;
+}
+
+template <int K>
+WM_DEV void copy_n(uint32_t (&r)[K], const uint32_t (&a)[K]) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = a[j];
+}
+
+template <int K>
+WM_DEV void zero_n(uint32_t (&r)[K]) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = 0u;
+}
+
+// r = (mask != 0) ? x : y, limb-wise select.
+template <int K>
+WM_DEV void select_n(uint32_t (&r)[K], uint32_t mask, const uint32_t (&x)[K], const uint32_t (&y)[K]) {
+#pragma unroll
+  for (int j = 0; j < K; ++j) r[j] = mask ? x[j] : y[j];
+}
+
+// a := (a >= m) ? a - m : a.  The ">=" (subtract on equality) convention is the
+// reference's canonical-residue rule (oracle.py:7-9).
+template <int K>
+WM_DEV void cond_sub(uint32_t (&a)[K], const uint32_t (&m)[K]) {
+  uint32_t d[K];
+  uint32_t br = sub_n<K>(d, a, m);
+  select_n<K>(a, br, a, d);
+}
+
+// Modular add of canonical inputs (reference _emit_addmod, kernels.py:122-128):
+// s = a + b; out = s < q ? s : s - q.  Requires q < 2^(32K-1) (the interface
+// bound q < 2^(bits-4) guarantees it), so s never overflows K limbs.
+template <int K>
+WM_DEV void add_mod(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K], const uint32_t (&q)[K]) {
+  uint32_t s[K];
+  add_n<K>(s, a, b);
+  cond_sub<K>(s, q);
+  copy_n<K>(r, s);
+}
+
+// Modular subtract of canonical inputs (reference _emit_submod, kernels.py:131-137):
+// d = a - b; out = a < b ? d + q : d.
+template <int K>
+WM_DEV void sub_mod(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K], const uint32_t (&q)[K]) {
+  uint32_t d[K], e[K];
+  uint32_t br = sub_n<K>(d, a, b);
+  add_n<K>(e, d, q);
+  select_n<K>(r, br, e, d);
+}
+
+// ------------------------------------------------------------------ products
+// t = a * b, full 2K-limb product (schoolbook, row scanning).  K^2 IMAD.WIDE.
+template <int K>
+WM_DEV void mul_full(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      uint64_t p = (uint64_t)a[j] * b[0] + c;
+      t[j] = (uint32_t)p;
+      c = (uint32_t)(p >> 32);
+    }
+    t[K] = c;
+  }
+#pragma unroll
+  for (int i = 1; i < K; ++i) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      uint64_t p = (uint64_t)a[j] * b[i] + t[i + j] + c;
+      t[i + j] = (uint32_t)p;
+      c = (uint32_t)(p >> 32);
+    }
+    t[i + K] = c;
+  }
+}
+
+// h ~= floor(a * b / 2^(32K)): the high half of the product, computed from the
+// columns >= C0 = K-2 only (partial products a_j*b_i with i+j < C0 and their
+// carries are dropped).  The neglected sum is < C0 * 2^(32(C0+1)) < 2^(32K-27),
+// so the result is the exact high half or one less.  K^2 - (K-2)(K-1)/2 products.
+template <int K>
+WM_DEV void mul_hi_trunc(uint32_t (&h)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  constexpr int C0 = (K > 2) ? K - 2 : 0;
+  constexpr int W = 2 * K - C0;  // columns C0 .. 2K-1
+  uint32_t acc[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) acc[j] = 0u;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const int j0 = (C0 - i) > 0 ? (C0 - i) : 0;
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (j < j0) continue;
+      uint64_t p = (uint64_t)a[j] * b[i] + acc[i + j - C0] + c;
+      acc[i + j - C0] = (uint32_t)p;
+      c = (uint32_t)(p >> 32);
+    }
+    acc[i + K - C0] = c;
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) h[j] = acc[K - C0 + j];
+}
+
+// r += a * b (mod 2^(32K)): only the partial products that land in the low K
+// limbs.  K(K-1)/2 IMAD.WIDE + K plain IMAD.
+template <int K>
+WM_DEV void mul_lo_acc(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j + i < K - 1; ++j) {
+      uint64_t p = (uint64_t)a[j] * b[i] + r[i + j] + c;
+      r[i + j] = (uint32_t)p;
+      c = (uint32_t)(p >> 32);
+    }
+    r[K - 1] += a[K - 1 - i] * b[i] + c;
+  }
+}
+
+// ------------------------------------------------------------------ Shoup
+// Multiply by a fixed operand w with precomputed wp = floor(w * 2^(32K) / p)
+// (Shoup / Harvey).  With np = 2^(32K) - p:
+//   qh = floor(v * wp / 2^(32K))  (truncated: true value or one less)
+//   r  = v*w + qh*np mod 2^(32K) = v*w - qh*p  in [0, 3p)
+// Requires v < 2^(32K) and w < p < 2^(32K-2).  Result is NOT reduced.
+template <int K>
+WM_DEV void mul_shoup_lazy(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
+                           const uint32_t (&wp)[K], const uint32_t (&np)[K]) {
+  uint32_t qh[K];
+  mul_hi_trunc<K>(qh, v, wp);
+  zero_n<K>(r);
+  mul_lo_acc<K>(r, v, w);
+  mul_lo_acc<K>(r, qh, np);
+}
+
+// Canonical Shoup multiply: v * w mod p in [0, p).
+template <int K>
+WM_DEV void mul_shoup(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
+                      const uint32_t (&wp)[K], const uint32_t (&p)[K], const uint32_t (&np)[K]) {
+  mul_shoup_lazy<K>(r, v, w, wp, np);
+  cond_sub<K>(r, p);
+  cond_sub<K>(r, p);
+}
+
+// ------------------------------------------------------------------ Barrett
+// Constants of a modulus q < 2^(32K-4) for the general multiply.  The modulus is
+// normalised to qn = q << s with 2^(M-1) <= qn < 2^M, M = 32K - 4, so that all
+// shifts inside the reduction are compile-time constants.  Host computes:
+//   mu8 = 8 * floor(2^(2M) / qn)   (< 2^(32K))
+//   nqn = 2^(32K) - qn,  qn2 = 2*qn
+template <int K>
+struct FieldConst {
+  uint32_t q[K];    // the modulus (canonical-residue bound)
+  uint32_t qn[K];   // q << s
+  uint32_t qn2[K];  // 2 * qn
+  uint32_t nqn[K];  // 2^(32K) - qn
+  uint32_t mu8[K];  // 8 * floor(2^(2M) / qn)
+  uint32_t s;       // normalisation shift, 0..31
+};
+
+template <int K>
+WM_DEV void shl_small(uint32_t (&r)[K], const uint32_t (&a)[K], uint32_t s) {
+#pragma unroll
+  for (int j = K - 1; j > 0; --j) r[j] = __funnelshift_l(a[j - 1], a[j], s);
+  r[0] = a[0] << s;
+}
+
+template <int K>
+WM_DEV void shr_small(uint32_t (&r)[K], const uint32_t (&a)[K], uint32_t s) {
+#pragma unroll
+  for (int j = 0; j < K - 1; ++j) r[j] = __funnelshift_r(a[j], a[j + 1], s);
+  r[K - 1] = a[K - 1] >> s;
+}
+
+// a * b mod q for canonical a, b.  Same Barrett quotient estimate as the
+// reference _emit_mulmod (kernels.py:140-153; oracle.barrett_mulmod
+// oracle.py:137-149): q1 = t >> (M-1), q3 = (q1*mu) >> (M+1), r = t - q3*q,
+// with the high product truncated and the low products limited to K limbs.
+// q3 is within 3 of the true quotient, so r < 4 qn and two conditional
+// subtractions (2qn, then qn) make it canonical.  Cost: K^2 + ~K^2/2 + K(K+1)/2
+// word products (reference lowering: 3 K^2).
+template <int K>
+WM_DEV void mul_barrett_pre(uint32_t (&r)[K], const uint32_t (&a_shifted)[K], const uint32_t (&b)[K],
+                            const FieldConst<K> &F) {
+  uint32_t t[2 * K];
+  mul_full<K>(t, a_shifted, b);
+  // q1 = t >> (M - 1) = t >> (32K - 5): limbs K-1 .. 2K-1 shifted by 27.
+  uint32_t q1[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) q1[j] = __funnelshift_r(t[K - 1 + j], (j + K < 2 * K) ? t[K + j] : 0u, 27);
+  uint32_t q3[K];
+  mul_hi_trunc<K>(q3, q1, F.mu8);
+  uint32_t rr[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) rr[j] = t[j];
+  mul_lo_acc<K>(rr, q3, F.nqn);
+  cond_sub<K>(rr, F.qn2);
+  cond_sub<K>(rr, F.qn);
+  shr_small<K>(r, rr, F.s);
+}
+
+template <int K>
+WM_DEV void mul_barrett(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K],
+                        const FieldConst<K> &F) {
+  uint32_t as[K];
+  shl_small<K>(as, a, F.s);
+  mul_barrett_pre<K>(r, as, b, F);
+}
+
+}  // namespace wm

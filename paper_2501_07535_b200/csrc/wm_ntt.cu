@@ -1,0 +1,658 @@
+// Radix-2 Cooley-Tukey NTT / INTT over K-limb prime fields.
+//
+// Reference semantics: run_ntt (kernels.py:483-499) — bit-reversed input,
+// DIT stages with span m = 2..n and twiddle root^(j*n/m) (butterfly_schedule,
+// kernels.py:395-413), butterfly (u + v*w, u - v*w) (build_ntt,
+// kernels.py:270-311), inverse = root_inv twiddles then a scale by n^-1
+// (kernels.py:496-498).  The output is the plain cyclic DFT
+// y[k] = sum_j x[j] root^(jk) mod p (ntt_reference, oracle.py:262-282), so any
+// exact factorisation of that DFT is bit-identical as long as every output
+// is a canonical residue.
+//
+// Reference GPU form: one global kernel launch per stage with __constant__
+// twiddles (emit.py:487-560), which ptxas rejects for n >= 2^12 at 256 bits.
+//
+// B200 design:
+//   * The n-point transform is factored into P <= 3 passes of L-point
+//     sub-transforms (four-step / Bailey, recursively for P = 3), each small
+//     enough that a CTA holds G whole lines in shared memory.
+//   * A pass loads its G lines with coalesced vector loads (G consecutive
+//     columns of element-contiguous values), scatters them bit-reversed into
+//     shared memory, runs log2(L) radix-2 DIT stages there (Shoup multiply
+//     against a shared-memory twiddle table), applies the inter-pass twiddle
+//     root^(e) in the store epilogue, and writes with coalesced vector stores.
+//   * Twiddles are generated on the device once per plan as (w, w') pairs,
+//     w' = floor(w * 2^(32K) / p), so each butterfly multiply is a Shoup
+//     multiply (~K^2 + K^2/2 word products instead of the reference's 3K^2).
+//   * For the inverse, n^-1 is folded into the last column pass's twiddle
+//     table (one-pass plans multiply by n^-1 in the epilogue instead).
+#include <algorithm>
+#include <cstdio>
+
+#include "wm_internal.cuh"
+#include "wm_io.cuh"
+
+namespace wm {
+
+template <int K>
+struct NttConst {
+  uint32_t p[K];
+  uint32_t np[K];   // 2^(32K) - p
+  uint32_t sc[K];   // n^-1            (one-pass inverse epilogue)
+  uint32_t scp[K];  // its Shoup companion
+};
+
+struct PassDesc {
+  int64_t n;
+  int logL;
+  int G;
+  int64_t lines_inner, lines_outer;
+  int64_t RO, RT, WO, WK;
+  int SH;
+  int64_t C1, C2, C3;
+  int scale_out;
+  int64_t tw_stride;  // n / L
+  int64_t total_lines;  // row passes: batch * lines_inner
+};
+
+// ------------------------------------------------------------------ in-smem DFT
+// G lines of L elements at data[(g*L + pos)*K], bit-reversed order on entry,
+// natural order on exit.  tw[e] (e < L/2) = (w, w') for w = root_L^e.
+template <int K>
+__device__ __forceinline__ void dft_stages(uint32_t *data, const uint32_t *tw, int logL, int G,
+                                           const NttConst<K> &c) {
+  const int L = 1 << logL;
+  const int half_total = G << (logL - 1);
+  for (int s = 0; s < logL; ++s) {
+    const int half = 1 << s;
+    for (int bf = threadIdx.x; bf < half_total; bf += blockDim.x) {
+      const int g = bf >> (logL - 1);
+      const int jj = bf & ((L >> 1) - 1);
+      const int j = jj & (half - 1);
+      const int p0 = ((jj >> s) << (s + 1)) + j;
+      uint32_t *e0 = data + (g * L + p0) * K;
+      uint32_t *e1 = e0 + half * K;
+      uint32_t u[K], v[K], t[K];
+      lds_elem<K>(u, e0);
+      lds_elem<K>(v, e1);
+      if (s == 0) {
+        copy_n<K>(t, v);  // root^0 = 1
+      } else {
+        uint32_t w[K], wp[K];
+        const uint32_t *te = tw + (j << (logL - 1 - s)) * (2 * K);
+        lds_elem<K>(w, te);
+        lds_elem<K>(wp, te + K);
+        mul_shoup<K>(t, v, w, wp, c.p, c.np);
+      }
+      uint32_t o0[K], o1[K];
+      add_mod<K>(o0, u, t, c.p);
+      sub_mod<K>(o1, u, t, c.p);
+      sts_elem<K>(e0, o0);
+      sts_elem<K>(e1, o1);
+    }
+    __syncthreads();
+  }
+}
+
+template <int K>
+__device__ __forceinline__ void load_subtw(uint32_t *tw, const uint32_t *table, int logL, int64_t stride) {
+  const int half = 1 << (logL - 1);
+  for (int idx = threadIdx.x; idx < half * 2; idx += blockDim.x) {
+    const int e = idx >> 1, part = idx & 1;
+    uint32_t v[K];
+    ldg_elem<K>(v, table + ((int64_t)e * stride) * (2 * K) + part * K);
+    sts_elem<K>(tw + e * (2 * K) + part * K, v);
+  }
+}
+
+// ------------------------------------------------------------------ column pass
+// Line (o, i), i in [0, lines_inner) consecutive per CTA (G of them).
+template <int K>
+__global__ void __launch_bounds__(256) ntt_col_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
+                                                    const uint32_t *tw_out, const __grid_constant__ PassDesc d,
+                                                    const __grid_constant__ NttConst<K> c) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int logL = d.logL, L = 1 << logL, G = d.G;
+  uint32_t *data = smem;
+  uint32_t *tw = smem + (size_t)G * L * K;
+  const int64_t tiles_inner = d.lines_inner / G;
+  const int64_t tile = blockIdx.x;
+  const int64_t o = tile / tiles_inner;
+  const int64_t i0 = (tile - o * tiles_inner) * G;
+  const int64_t base = (int64_t)blockIdx.y * d.n;
+
+  load_subtw<K>(tw, tw_sub, logL, d.tw_stride);
+  for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
+    const int t = idx / G, g = idx - t * G;
+    const int64_t pos = base + o * d.RO + (int64_t)t * d.RT + i0 + g;
+    uint32_t v[K];
+    ldg_elem<K>(v, in + pos * K);
+    const int tb = (int)(__brev((unsigned)t) >> (32 - logL));
+    sts_elem<K>(data + (g * L + tb) * K, v);
+  }
+  __syncthreads();
+  dft_stages<K>(data, tw, logL, G, c);
+  const int64_t nmask = d.n - 1;
+  for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
+    const int k = idx / G, g = idx - k * G;
+    uint32_t v[K];
+    lds_elem<K>(v, data + (g * L + k) * K);
+    if (d.C3) {
+      const int64_t e = ((((i0 + g) >> d.SH) * (o * d.C1 + (int64_t)k * d.C2)) * d.C3) & nmask;
+      uint32_t w[K], wp[K], r[K];
+      ldg_elem<K>(w, tw_out + e * (2 * K));
+      ldg_elem<K>(wp, tw_out + e * (2 * K) + K);
+      mul_shoup<K>(r, v, w, wp, c.p, c.np);
+      copy_n<K>(v, r);
+    }
+    const int64_t pos = base + o * d.WO + (int64_t)k * d.WK + i0 + g;
+    stg_elem<K>(out + pos * K, v);
+  }
+}
+
+// ------------------------------------------------------------------ row pass
+// Line lambda in [0, batch * lines_inner): b = lambda / R, r = lambda % R.
+template <int K>
+__global__ void __launch_bounds__(256) ntt_row_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
+                                                    const __grid_constant__ PassDesc d,
+                                                    const __grid_constant__ NttConst<K> c) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const int logL = d.logL, L = 1 << logL, G = d.G;
+  uint32_t *data = smem;
+  uint32_t *tw = smem + (size_t)G * L * K;
+  const int64_t lam0 = (int64_t)blockIdx.x * G;
+
+  load_subtw<K>(tw, tw_sub, logL, d.tw_stride);
+  for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
+    const int g = idx >> logL, t = idx & (L - 1);
+    const int64_t lam = lam0 + g;
+    if (lam < d.total_lines) {
+      const int64_t b = lam / d.lines_inner, r = lam - b * d.lines_inner;
+      const int64_t pos = b * d.n + r * L + t;
+      uint32_t v[K];
+      ldg_elem<K>(v, in + pos * K);
+      const int tb = (int)(__brev((unsigned)t) >> (32 - logL));
+      sts_elem<K>(data + (g * L + tb) * K, v);
+    }
+  }
+  __syncthreads();
+  dft_stages<K>(data, tw, logL, G, c);
+  for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
+    const int g = idx >> logL, k = idx & (L - 1);
+    const int64_t lam = lam0 + g;
+    if (lam < d.total_lines) {
+      const int64_t b = lam / d.lines_inner, r = lam - b * d.lines_inner;
+      uint32_t v[K];
+      lds_elem<K>(v, data + (g * L + k) * K);
+      if (d.scale_out) {
+        uint32_t rr[K];
+        mul_shoup<K>(rr, v, c.sc, c.scp, c.p, c.np);
+        copy_n<K>(v, rr);
+      }
+      const int64_t pos = b * d.n + r * d.WO + (int64_t)k * d.WK;
+      stg_elem<K>(out + pos * K, v);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ twiddles
+template <int K>
+struct TwGenArgs {
+  FieldConst<K> F;  // Barrett constants of p
+  uint32_t base[K];
+  uint32_t scale[K];
+  int64_t chunk;
+};
+
+// wp = floor(w * 2^(32K) / p) by binary long division (w < p < 2^(32K-4)).
+template <int K>
+__device__ void shoup_companion(uint32_t (&wp)[K], const uint32_t (&w)[K], const uint32_t (&p)[K]) {
+  uint32_t rem[K];
+  copy_n<K>(rem, w);
+#pragma unroll
+  for (int limb = K - 1; limb >= 0; --limb) {
+    uint32_t qw = 0;
+    for (int b = 31; b >= 0; --b) {
+      uint32_t sh[K];
+      shl_small<K>(sh, rem, 1u);
+      uint32_t d[K];
+      uint32_t br = sub_n<K>(d, sh, p);
+      select_n<K>(rem, br, sh, d);
+      qw = (qw << 1) | (br ? 0u : 1u);
+    }
+    wp[limb] = qw;
+  }
+}
+
+template <int K>
+__global__ void twiddle_gen_kernel(uint32_t *table, int64_t count, const __grid_constant__ TwGenArgs<K> a) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t e0 = t * a.chunk;
+  if (e0 >= count) return;
+  uint32_t x[K], b[K];
+  copy_n<K>(x, a.scale);
+  copy_n<K>(b, a.base);
+  for (int64_t e = e0; e; e >>= 1) {
+    uint32_t r[K];
+    if (e & 1) {
+      mul_barrett<K>(r, x, b, a.F);
+      copy_n<K>(x, r);
+    }
+    mul_barrett<K>(r, b, b, a.F);
+    copy_n<K>(b, r);
+  }
+  const int64_t e1 = (e0 + a.chunk < count) ? e0 + a.chunk : count;
+  for (int64_t e = e0; e < e1; ++e) {
+    uint32_t wp[K];
+    shoup_companion<K>(wp, x, a.F.q);
+    stg_elem<K>(table + e * (2 * K), x);
+    stg_elem<K>(table + e * (2 * K) + K, wp);
+    uint32_t r[K];
+    mul_barrett<K>(r, x, a.base, a.F);
+    copy_n<K>(x, r);
+  }
+}
+
+template <int K>
+__global__ void twiddle_extract_kernel(const uint32_t *table, int64_t count, uint32_t *out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += stride) {
+    uint32_t v[K];
+    ldg_elem<K>(v, table + e * (2 * K));
+    for (int j = 0; j < K; ++j) out[e * K + j] = v[j];
+  }
+}
+
+// ------------------------------------------------------------------ host side
+template <int K>
+static FieldConst<K> field_const_local(const wm_field *f) {
+  FieldConst<K> c;
+  for (int j = 0; j < K; ++j) {
+    c.q[j] = f->q[j];
+    c.qn[j] = f->qn[j];
+    c.qn2[j] = f->qn2[j];
+    c.nqn[j] = f->nqn[j];
+    c.mu8[j] = f->mu8[j];
+  }
+  c.s = (uint32_t)f->s;
+  return c;
+}
+
+template <int K>
+static int gen_table(const wm_field *f, uint32_t *table, int64_t count, const Big &base, const Big &scale) {
+  TwGenArgs<K> a;
+  a.F = field_const_local<K>(f);
+  for (int j = 0; j < K; ++j) {
+    a.base[j] = base[j];
+    a.scale[j] = scale[j];
+  }
+  a.chunk = 64;
+  int64_t threads = (count + a.chunk - 1) / a.chunk;
+  int grid = (int)((threads + 127) / 128);
+  twiddle_gen_kernel<K><<<grid, 128>>>(table, count, a);
+  WM_LAUNCH_CHECK("twiddle_gen launch");
+  return WM_OK;
+}
+
+template <int K>
+static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
+  NttConst<K> c;
+  for (int j = 0; j < K; ++j) {
+    c.p[j] = pl->field->q[j];
+    c.np[j] = pl->np[j];
+    c.sc[j] = pl->ninv[j];
+    c.scp[j] = pl->ninv_sh[j];
+  }
+  return c;
+}
+
+static size_t pass_smem(int K, const wm_ntt_pass &ps) {
+  const size_t L = (size_t)1 << ps.logL;
+  return ((size_t)ps.G * L * K + (L / 2) * 2 * K) * sizeof(uint32_t);
+}
+
+template <int K>
+static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
+                      uint32_t *ws, cudaStream_t st) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    WM_CUDA_TRY(cudaFuncSetAttribute(ntt_col_pass<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    WM_CUDA_TRY(cudaFuncSetAttribute(ntt_row_pass<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_done = true;
+  }
+  const NttConst<K> c = ntt_const<K>(pl);
+  const uint32_t *tw_sub = inverse ? pl->tw_inv : pl->tw_fwd;
+  for (const wm_ntt_pass &ps : pl->passes) {
+    const uint32_t *src = ps.src == 0 ? in : (ps.src == 1 ? ws : out);
+    uint32_t *dst = ps.dst == 0 ? out : ws;
+    PassDesc d;
+    d.n = pl->n;
+    d.logL = ps.logL;
+    d.G = ps.G;
+    d.lines_inner = ps.lines_inner;
+    d.lines_outer = ps.lines_outer;
+    d.RO = ps.RO;
+    d.RT = ps.RT;
+    d.WO = ps.WO;
+    d.WK = ps.WK;
+    d.SH = ps.SH;
+    d.C1 = ps.C1;
+    d.C2 = ps.C2;
+    d.C3 = ps.C3;
+    d.scale_out = (inverse && ps.scale_out) ? 1 : 0;
+    d.tw_stride = pl->n >> ps.logL;
+    d.total_lines = batch * ps.lines_inner;
+    const size_t smem = pass_smem(K, ps);
+    if (ps.column) {
+      const uint32_t *tw_out = inverse ? (ps.scaled_table ? pl->tw_inv_scaled : pl->tw_inv) : pl->tw_fwd;
+      dim3 grid((unsigned)(ps.lines_outer * (ps.lines_inner / ps.G)), (unsigned)batch);
+      ntt_col_pass<K><<<grid, 256, smem, st>>>(src, dst, tw_sub, tw_out, d, c);
+      WM_LAUNCH_CHECK("ntt_col_pass launch");
+    } else {
+      const int64_t lines = batch * ps.lines_inner;
+      dim3 grid((unsigned)((lines + ps.G - 1) / ps.G));
+      ntt_row_pass<K><<<grid, 256, smem, st>>>(src, dst, tw_sub, d, c);
+      WM_LAUNCH_CHECK("ntt_row_pass launch");
+    }
+  }
+  return WM_OK;
+}
+
+static int plan_passes(wm_ntt_plan *pl) {
+  const int K = pl->K;
+  const int logn = pl->logn;
+  // largest sub-transform whose line fits in <= 96 KB of shared memory
+  int logLmax = 1;
+  while (logLmax < 11 && ((size_t)2 << logLmax) * K * 4 <= 96 * 1024) ++logLmax;
+  const int P = (logn + logLmax - 1) / logLmax;
+  if (P > 3) return fail(WM_EUNSUPPORTED, "transform too long for three passes at this width");
+  std::vector<int> sizes(P, logn / P);
+  for (int i = 0; i < logn % P; ++i) sizes[i] += 1;
+  auto choose_G = [&](int logL, int64_t inner_cap) {
+    int64_t words_line = ((int64_t)1 << logL) * K;
+    int64_t G = std::max<int64_t>(1, 16384 / words_line);  // ~64 KB of data per CTA
+    G = std::min<int64_t>(G, 32);
+    int64_t g = 1;
+    while (g * 2 <= G) g *= 2;
+    return (int)std::min<int64_t>(g, inner_cap);
+  };
+  pl->passes.clear();
+  const int64_t n = pl->n;
+  if (P == 1) {
+    wm_ntt_pass a;
+    a.column = false;
+    a.logL = logn;
+    a.G = choose_G(logn, 1 << 20);
+    a.lines_inner = 1;
+    a.WO = n;
+    a.WK = 1;
+    a.scale_out = true;
+    a.src = 0;
+    a.dst = 0;
+    pl->passes.push_back(a);
+  } else if (P == 2) {
+    const int logN2 = sizes[0], logN1 = sizes[1];
+    const int64_t N1 = (int64_t)1 << logN1, N2 = (int64_t)1 << logN2;
+    wm_ntt_pass a;  // N2-point DFTs over j2 (stride N1), twiddle root^(j1*k2)
+    a.column = true;
+    a.logL = logN2;
+    a.G = choose_G(logN2, N1);
+    a.lines_inner = N1;
+    a.lines_outer = 1;
+    a.RO = 0;
+    a.RT = N1;
+    a.WO = 0;
+    a.WK = N1;
+    a.SH = 0;
+    a.C1 = 0;
+    a.C2 = 1;
+    a.C3 = 1;
+    a.scaled_table = true;
+    a.src = 0;
+    a.dst = 1;
+    wm_ntt_pass b;  // N1-point DFTs over contiguous j1, transposing store
+    b.column = false;
+    b.logL = logN1;
+    b.G = choose_G(logN1, 1 << 20);
+    b.lines_inner = N2;
+    b.WO = 1;
+    b.WK = N2;
+    b.src = 1;
+    b.dst = 0;
+    pl->passes.push_back(a);
+    pl->passes.push_back(b);
+  } else {
+    const int logM2 = sizes[0], logM1 = sizes[1], logN1 = sizes[2];
+    const int64_t N1 = (int64_t)1 << logN1, M1 = (int64_t)1 << logM1, M2 = (int64_t)1 << logM2;
+    const int64_t N2 = M1 * M2;
+    wm_ntt_pass a;  // M2-point DFTs over b, lines i = j1 + N1*a; twiddle root^(N1*a*c)
+    a.column = true;
+    a.logL = logM2;
+    a.G = choose_G(logM2, N1 * M1);
+    a.lines_inner = N1 * M1;
+    a.lines_outer = 1;
+    a.RT = N1 * M1;
+    a.WK = N1 * M1;
+    a.SH = logN1;
+    a.C1 = 0;
+    a.C2 = 1;
+    a.C3 = N1;
+    a.scaled_table = false;
+    a.src = 0;
+    a.dst = 0;
+    wm_ntt_pass b;  // M1-point DFTs over a, lines (o=c, i=j1); twiddle root^(j1*(c + M2*d))
+    b.column = true;
+    b.logL = logM1;
+    b.G = choose_G(logM1, N1);
+    b.lines_inner = N1;
+    b.lines_outer = M2;
+    b.RO = N1 * M1;
+    b.RT = N1;
+    b.WO = N1;
+    b.WK = N1 * M2;
+    b.SH = 0;
+    b.C1 = 1;
+    b.C2 = M2;
+    b.C3 = 1;
+    b.scaled_table = true;
+    b.src = 2;  // reads `out` (written by pass a)
+    b.dst = 1;
+    wm_ntt_pass cc;  // N1-point DFTs over contiguous j1, transposing store
+    cc.column = false;
+    cc.logL = logN1;
+    cc.G = choose_G(logN1, 1 << 20);
+    cc.lines_inner = N2;
+    cc.WO = 1;
+    cc.WK = N2;
+    cc.src = 1;
+    cc.dst = 0;
+    pl->passes.push_back(a);
+    pl->passes.push_back(b);
+    pl->passes.push_back(cc);
+  }
+  for (const auto &ps : pl->passes) {
+    if (pass_smem(K, ps) > 227 * 1024) return fail(WM_EUNSUPPORTED, "pass does not fit in shared memory");
+  }
+  return WM_OK;
+}
+
+template <int K>
+static int create_tables(wm_ntt_plan *pl, const Big &root, const Big &root_inv) {
+  const int64_t n = pl->n;
+  const size_t bytes = (size_t)n * 2 * K * sizeof(uint32_t);
+  WM_CUDA_TRY(cudaMalloc(&pl->tw_fwd, bytes));
+  WM_CUDA_TRY(cudaMalloc(&pl->tw_inv, bytes));
+  Big one(K, 0u);
+  one[0] = 1;
+  int rc = gen_table<K>(pl->field, pl->tw_fwd, n, root, one);
+  if (rc) return rc;
+  rc = gen_table<K>(pl->field, pl->tw_inv, n, root_inv, one);
+  if (rc) return rc;
+  if (pl->passes.size() > 1) {
+    WM_CUDA_TRY(cudaMalloc(&pl->tw_inv_scaled, bytes));
+    rc = gen_table<K>(pl->field, pl->tw_inv_scaled, n, root_inv, pl->ninv);
+    if (rc) return rc;
+  }
+  WM_CUDA_TRY(cudaDeviceSynchronize());
+  return WM_OK;
+}
+
+}  // namespace wm
+
+using namespace wm;
+
+extern "C" {
+
+int wm_ntt_plan_create(const wm_field *f, int64_t n, const uint32_t *root_host, const uint32_t *root_inv_host,
+                       const uint32_t *n_inv_host, wm_ntt_plan **out) {
+  if (!out) return fail(WM_EINVAL, "null output pointer");
+  *out = nullptr;
+  if (!f) return fail(WM_EINVAL, "null field");
+  if (!root_host || !root_inv_host || !n_inv_host) return fail(WM_EINVAL, "null root/root_inv/n_inv");
+  if (n < 2 || (n & (n - 1))) return fail(WM_EINVAL, "transform length must be a power of two >= 2");
+  if (n > ((int64_t)1 << 30)) return fail(WM_EUNSUPPORTED, "transform length above 2^30");
+  const int K = f->K;
+  if (!ntt_supports(K)) return fail(WM_EUNSUPPORTED, "limb count not built into the NTT kernels");
+  // Shoup needs p < 2^(32K-2): guaranteed by the field's p < 2^(32K-4).
+  wm_ntt_plan *pl = new wm_ntt_plan();
+  pl->field = f;
+  pl->K = K;
+  pl->n = n;
+  pl->logn = 63 - __builtin_clzll((unsigned long long)n);
+  Big root(root_host, root_host + K), root_inv(root_inv_host, root_inv_host + K);
+  pl->ninv = Big(n_inv_host, n_inv_host + K);
+  // Shoup companion of n^-1 and np = 2^(32K) - p on the host.
+  {
+    Big num = big_shl(pl->ninv, 32 * K, 2 * K);
+    // floor(num / p) via long division over 64K bits
+    Big rem(K + 1, 0u), dd = big_resize(f->q, K + 1), quo(K, 0u);
+    for (int bit = 64 * K - 1; bit >= 0; --bit) {
+      uint32_t carry = (num[bit / 32] >> (bit % 32)) & 1u;
+      for (int j = 0; j < K + 1; ++j) {
+        uint32_t nc = rem[j] >> 31;
+        rem[j] = (rem[j] << 1) | carry;
+        carry = nc;
+      }
+      if (big_ge(rem, dd)) {
+        big_sub_inplace(rem, dd);
+        if (bit / 32 < K) quo[bit / 32] |= 1u << (bit % 32);
+      }
+    }
+    pl->ninv_sh = quo;
+    pl->np = Big(K, 0u);
+    big_sub_inplace(pl->np, f->q);
+  }
+  int rc = plan_passes(pl);
+  if (rc) {
+    delete pl;
+    return rc;
+  }
+  switch (K) {
+#define WM_CASE(k)                                  \
+  case k:                                           \
+    rc = create_tables<k>(pl, root, root_inv);      \
+    break;
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      rc = fail(WM_EUNSUPPORTED, "limb count not built into the NTT kernels");
+  }
+  if (rc) {
+    wm_ntt_plan_destroy(pl);
+    return rc;
+  }
+  *out = pl;
+  return WM_OK;
+}
+
+int wm_ntt_plan_destroy(wm_ntt_plan *p) {
+  if (!p) return WM_OK;
+  if (p->tw_fwd) cudaFree(p->tw_fwd);
+  if (p->tw_inv) cudaFree(p->tw_inv);
+  if (p->tw_inv_scaled) cudaFree(p->tw_inv_scaled);
+  if (p->ws) cudaFree(p->ws);
+  delete p;
+  return WM_OK;
+}
+
+int wm_ntt_plan_info(const wm_ntt_plan *p, int *passes, int *log_sizes, int cap) {
+  if (!p) return fail(WM_EINVAL, "null plan");
+  if (passes) *passes = (int)p->passes.size();
+  for (int i = 0; i < (int)p->passes.size() && i < cap; ++i) log_sizes[i] = p->passes[i].logL;
+  return WM_OK;
+}
+
+int64_t wm_ntt_workspace_bytes(const wm_ntt_plan *p, int64_t batch) {
+  if (!p || batch < 0) return -1;
+  if (p->passes.size() <= 1) return 0;
+  return batch * p->n * p->K * (int64_t)sizeof(uint32_t);
+}
+
+static int ntt_run(const wm_ntt_plan *pc, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
+                   void *workspace, void *stream) {
+  if (!pc) return fail(WM_EINVAL, "null plan");
+  if (batch < 0) return fail(WM_EINVAL, "negative batch");
+  if (batch == 0) return WM_OK;
+  if (!in || !out) return fail(WM_EINVAL, "null data pointer");
+  if (batch > 65535 && pc->passes.size() > 1) return fail(WM_EUNSUPPORTED, "batch above 65535 for multi-pass plans");
+  wm_ntt_plan *p = const_cast<wm_ntt_plan *>(pc);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t need = wm_ntt_workspace_bytes(p, batch);
+  std::unique_lock<std::mutex> lk(p->ws_mu, std::defer_lock);
+  uint32_t *ws = static_cast<uint32_t *>(workspace);
+  if (need > 0 && !ws) {
+    lk.lock();
+    if (p->ws_bytes < need) {
+      if (p->ws) {
+        WM_CUDA_TRY(cudaStreamSynchronize(st));
+        WM_CUDA_TRY(cudaFree(p->ws));
+        p->ws = nullptr;
+        p->ws_bytes = 0;
+      }
+      WM_CUDA_TRY(cudaMalloc(&p->ws, need));
+      p->ws_bytes = need;
+    }
+    ws = static_cast<uint32_t *>(p->ws);
+  }
+  switch (p->K) {
+#define WM_CASE(k) \
+  case k:          \
+    return run_passes<k>(p, inverse, in, out, batch, ws, st);
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      return fail(WM_EUNSUPPORTED, "limb count not built into the NTT kernels");
+  }
+}
+
+int wm_ntt_forward(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int64_t batch, void *workspace,
+                   void *stream) {
+  return ntt_run(p, false, in, out, batch, workspace, stream);
+}
+
+int wm_ntt_inverse(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int64_t batch, void *workspace,
+                   void *stream) {
+  return ntt_run(p, true, in, out, batch, workspace, stream);
+}
+
+int wm_ntt_twiddles(const wm_ntt_plan *p, int inverse, int64_t count, uint32_t *out, void *stream) {
+  if (!p) return fail(WM_EINVAL, "null plan");
+  if (count < 0 || count > p->n) return fail(WM_EINVAL, "count out of range");
+  if (count == 0) return WM_OK;
+  const uint32_t *table = inverse ? p->tw_inv : p->tw_fwd;
+  int grid = (int)std::min<int64_t>((count + 255) / 256, 148 * 8);
+  switch (p->K) {
+#define WM_CASE(k)                                                                             \
+  case k:                                                                                      \
+    twiddle_extract_kernel<k><<<grid, 256, 0, (cudaStream_t)stream>>>(table, count, out);      \
+    break;
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      return fail(WM_EUNSUPPORTED, "limb count not built into the NTT kernels");
+  }
+  WM_LAUNCH_CHECK("twiddle_extract launch");
+  return WM_OK;
+}
+
+}  // extern "C"

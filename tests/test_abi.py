@@ -1,0 +1,73 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every symbol the
+public header declares.  Only host-only entry points are called here (no
+kernel launches, no CUDA context needed)."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+from paper_2501_07535_b200 import _lib
+
+HEADER = Path(__file__).resolve().parent.parent / "include" / "widemod_b200.h"
+
+
+def declared_symbols() -> list[str]:
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(wm_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    return _lib.load()
+
+
+def test_header_symbols_exported(lib):
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for name in syms:
+        assert hasattr(lib, name), name
+    assert sorted(n for n, _, _ in _lib.SIGNATURES) == syms
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["cuobjdump", "--list-elf", str(_lib.LIB_PATH)], capture_output=True, text=True)
+    assert out.returncode == 0 and "sm_100a" in out.stdout
+
+
+def test_host_only_entry_points(lib):
+    assert lib.wm_abi_version() == 1
+    assert lib.wm_limbs_for_bits(256) == 8
+    assert lib.wm_limbs_for_bits(384) == 12
+    assert lib.wm_limbs_for_bits(768) == 24
+    assert lib.wm_limbs_for_bits(16) == 1
+    buf = (ctypes.c_int * 32)()
+    m = lib.wm_supported_limbs(1, buf, 32)
+    assert {1, 2, 4, 8, 12, 24} <= set(buf[:m])
+
+
+def test_field_create_validation(lib):
+    h = ctypes.c_void_p()
+    q = (ctypes.c_uint32 * 8)(*([0xFFFFFF7F] + [0xFFFFFFFF] * 6 + [0x0FFFFFFF]))  # 2^252 - 129
+    assert lib.wm_field_create(256, q, 8, ctypes.byref(h)) == _lib.WM_OK
+    b, k, s = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    assert lib.wm_field_info(h, ctypes.byref(b), ctypes.byref(k), ctypes.byref(s)) == 0
+    assert (b.value, k.value, s.value) == (256, 8, 0)
+    lib.wm_field_destroy(h)
+    # q = 500 at width 13 (reference test_kernels.py:31-33): normalisation shift 19
+    q500 = (ctypes.c_uint32 * 1)(500)
+    assert lib.wm_field_create(13, q500, 1, ctypes.byref(h)) == 0
+    assert lib.wm_field_info(h, ctypes.byref(b), ctypes.byref(k), ctypes.byref(s)) == 0
+    assert (k.value, s.value) == (1, 19)
+    lib.wm_field_destroy(h)
+    one = (ctypes.c_uint32 * 1)(1)
+    assert lib.wm_field_create(16, one, 1, ctypes.byref(h)) == _lib.WM_EINVAL
+    assert b"exceed" in lib.wm_last_error()
+    big = (ctypes.c_uint32 * 1)(0xFFFFFFFF)
+    assert lib.wm_field_create(32, big, 1, ctypes.byref(h)) == _lib.WM_EINVAL
+    assert lib.wm_field_create(4000, one, 1, ctypes.byref(h)) == _lib.WM_EUNSUPPORTED
