@@ -74,6 +74,7 @@ struct wm_ntt_pass {
   int64_t C1 = 0, C2 = 0, C3 = 0;
   bool scaled_table = false;  // inverse: use the n^-1-scaled table for this pass
   bool scale_out = false;     // inverse one-pass plans: multiply outputs by n^-1
+  bool canonical_out = false; // last pass of the transform: [0, 4p) -> [0, p)
   int src = 0, dst = 0;       // 0 = user in/out, 1 = workspace (see plan creation)
 };
 
@@ -85,7 +86,7 @@ struct wm_ntt_plan {
   std::vector<wm_ntt_pass> passes;
   // device tables: n entries of (w, w') pairs (2K words each)
   uint32_t *tw_fwd = nullptr, *tw_inv = nullptr, *tw_inv_scaled = nullptr;
-  wm::Big ninv, ninv_sh, np;  // n^-1, floor(n^-1 * 2^32K / p), 2^32K - p
+  wm::Big ninv, ninv_sh, np, p2;  // n^-1, floor(n^-1 * 2^32K / p), 2^32K - p, 2p
   // internal workspace (used when the caller passes none)
   std::mutex ws_mu;
   void *ws = nullptr;

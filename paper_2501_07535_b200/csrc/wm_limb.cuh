@@ -106,30 +106,56 @@ WM_DEV void sub_mod(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b
 }
 
 // ------------------------------------------------------------------ products
+// Products are formed with mul.wide.u32 (one IMAD.WIDE, 32x32->64) and the
+// two 32-bit halves are folded into the accumulator with add.cc/addc chains
+// (IADD3 with carry predicates on the ALU pipe): per word product one
+// FMA-heavy instruction and two ALU instructions, which keeps the two pipes
+// balanced (profiles/r01_shoup_rate.jsonl: 2x faster than compiler-chosen
+// carry code at K = 24, on par at K = 8).
+WM_DEV uint64_t mul_wide(uint32_t a, uint32_t b) {
+  uint64_t r;
+  asm("mul.wide.u32 %0, %1, %2;" : "=l"(r) : "r"(a), "r"(b));
+  return r;
+}
+WM_DEV uint32_t lo32(uint64_t x) { return (uint32_t)x; }
+WM_DEV uint32_t hi32(uint64_t x) { return (uint32_t)(x >> 32); }
+
+// One row of a row-scanning schoolbook product:
+//   acc[base .. base+K] += a[j0..K) * b << 32*(j - j0 + ...)  i.e.
+//   acc[base + j] += lo(a_j b), acc[base + j + 1] += hi(a_j b) for j in [j0, K).
+// acc[base + K] must be zero on entry; no carry leaves acc[base + K] (the
+// callers' partial sums fit).  base, j0 are compile-time after unrolling.
+template <int K, int N>
+WM_DEV void mac_row(uint32_t (&acc)[N], const int base, const uint32_t (&a)[K], const uint32_t b, const int j0) {
+  uint64_t p[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    if (j >= j0) p[j] = mul_wide(a[j], b);
+  // low halves, carry into acc[base + K]
+  asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(acc[base + j0]) : "r"(lo32(p[j0])));
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+    if (j > j0) asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(acc[base + j]) : "r"(lo32(p[j])));
+  asm volatile("addc.u32 %0, 0, 0;" : "=r"(acc[base + K]));
+  // high halves, one limb up
+  if (j0 == K - 1) {
+    asm volatile("add.u32 %0, %0, %1;" : "+r"(acc[base + K]) : "r"(hi32(p[K - 1])));
+  } else {
+    asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(acc[base + j0 + 1]) : "r"(hi32(p[j0])));
+#pragma unroll
+    for (int j = 0; j < K - 1; ++j)
+      if (j > j0) asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(acc[base + j + 1]) : "r"(hi32(p[j])));
+    asm volatile("addc.u32 %0, %0, %1;" : "+r"(acc[base + K]) : "r"(hi32(p[K - 1])));
+  }
+}
+
 // t = a * b, full 2K-limb product (schoolbook, row scanning).  K^2 IMAD.WIDE.
 template <int K>
 WM_DEV void mul_full(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
-  {
-    uint32_t c = 0;
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      uint64_t p = (uint64_t)a[j] * b[0] + c;
-      t[j] = (uint32_t)p;
-      c = (uint32_t)(p >> 32);
-    }
-    t[K] = c;
-  }
+  for (int j = 0; j < 2 * K; ++j) t[j] = 0u;
 #pragma unroll
-  for (int i = 1; i < K; ++i) {
-    uint32_t c = 0;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-      uint64_t p = (uint64_t)a[j] * b[i] + t[i + j] + c;
-      t[i + j] = (uint32_t)p;
-      c = (uint32_t)(p >> 32);
-    }
-    t[i + K] = c;
-  }
+  for (int i = 0; i < K; ++i) mac_row<K, 2 * K>(t, i, a, b[i], 0);
 }
 
 // h ~= floor(a * b / 2^(32K)): the high half of the product, computed from the
@@ -139,41 +165,73 @@ WM_DEV void mul_full(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_
 template <int K>
 WM_DEV void mul_hi_trunc(uint32_t (&h)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
   constexpr int C0 = (K > 2) ? K - 2 : 0;
-  constexpr int W = 2 * K - C0;  // columns C0 .. 2K-1
-  uint32_t acc[W];
+  constexpr int W = 2 * K - C0;  // columns C0 .. 2K-1, acc[c - C0]
+  uint32_t acc[W + 1];
 #pragma unroll
-  for (int j = 0; j < W; ++j) acc[j] = 0u;
+  for (int j = 0; j <= W; ++j) acc[j] = 0u;
+  // rows i < C0 start at column C0 (j0 = C0 - i); their acc base is 0 with
+  // the row shifted: column i + j  ->  acc[i + j - C0]
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    const int j0 = (C0 - i) > 0 ? (C0 - i) : 0;
-    uint32_t c = 0;
+    if (i < C0) {
+      // acc[(i + j) - C0] for j >= C0 - i: same as mac_row on a shifted view
+      const int j0 = C0 - i;
+      uint64_t p[K];
 #pragma unroll
-    for (int j = 0; j < K; ++j) {
-      if (j < j0) continue;
-      uint64_t p = (uint64_t)a[j] * b[i] + acc[i + j - C0] + c;
-      acc[i + j - C0] = (uint32_t)p;
-      c = (uint32_t)(p >> 32);
+      for (int j = 0; j < K; ++j)
+        if (j >= j0) p[j] = mul_wide(a[j], b[i]);
+      asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(acc[0]) : "r"(lo32(p[j0])));
+#pragma unroll
+      for (int j = 0; j < K; ++j)
+        if (j > j0) asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(acc[i + j - C0]) : "r"(lo32(p[j])));
+      asm volatile("addc.u32 %0, 0, 0;" : "=r"(acc[i + K - C0]));
+      if (j0 == K - 1) {
+        asm volatile("add.u32 %0, %0, %1;" : "+r"(acc[i + K - C0]) : "r"(hi32(p[K - 1])));
+      } else {
+        asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(acc[1]) : "r"(hi32(p[j0])));
+#pragma unroll
+        for (int j = 0; j < K - 1; ++j)
+          if (j > j0) asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(acc[i + j + 1 - C0]) : "r"(hi32(p[j])));
+        asm volatile("addc.u32 %0, %0, %1;" : "+r"(acc[i + K - C0]) : "r"(hi32(p[K - 1])));
+      }
+    } else {
+      mac_row<K, W + 1>(acc, i - C0, a, b[i], 0);
     }
-    acc[i + K - C0] = c;
   }
 #pragma unroll
   for (int j = 0; j < K; ++j) h[j] = acc[K - C0 + j];
 }
 
 // r += a * b (mod 2^(32K)): only the partial products that land in the low K
-// limbs.  K(K-1)/2 IMAD.WIDE + K plain IMAD.
+// limbs.  K(K-1)/2 IMAD.WIDE + K plain IMAD (the top column's low halves).
 template <int K>
 WM_DEV void mul_lo_acc(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    uint32_t c = 0;
-#pragma unroll
-    for (int j = 0; j + i < K - 1; ++j) {
-      uint64_t p = (uint64_t)a[j] * b[i] + r[i + j] + c;
-      r[i + j] = (uint32_t)p;
-      c = (uint32_t)(p >> 32);
+    const int m = K - i;  // a_0 .. a_{m-1} reach limbs i .. K-1
+    const uint32_t last = a[m - 1] * b[i];
+    if (m == 1) {
+      r[K - 1] += last;
+      continue;
     }
-    r[K - 1] += a[K - 1 - i] * b[i] + c;
+    uint64_t p[K];
+#pragma unroll
+    for (int j = 0; j < K; ++j)
+      if (j < m - 1) p[j] = mul_wide(a[j], b[i]);
+    asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(r[i]) : "r"(lo32(p[0])));
+#pragma unroll
+    for (int j = 1; j < K; ++j)
+      if (j < m - 1) asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(r[i + j]) : "r"(lo32(p[j])));
+    asm volatile("addc.u32 %0, %0, %1;" : "+r"(r[K - 1]) : "r"(last));
+    if (m == 2) {
+      r[K - 1] += hi32(p[0]);
+    } else {
+      asm volatile("add.cc.u32 %0, %0, %1;" : "+r"(r[i + 1]) : "r"(hi32(p[0])));
+#pragma unroll
+      for (int j = 1; j < K; ++j)
+        if (j < m - 2) asm volatile("addc.cc.u32 %0, %0, %1;" : "+r"(r[i + j + 1]) : "r"(hi32(p[j])));
+      asm volatile("addc.u32 %0, %0, %1;" : "+r"(r[K - 1]) : "r"(hi32(p[m - 2])));
+    }
   }
 }
 
@@ -200,6 +258,49 @@ WM_DEV void mul_shoup(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (
   mul_shoup_lazy<K>(r, v, w, wp, np);
   cond_sub<K>(r, p);
   cond_sub<K>(r, p);
+}
+
+// ------------------------------------------------------------------ lazy butterflies
+// Harvey-style lazy reduction for the NTT: values live in [0, 4p) between
+// stages and passes (4p < 2^(32K) because p < 2^(32K-4)); only the last pass
+// of a transform makes them canonical.
+//   t  = shoup_lazy(v)            in [0, 3p)  -> cond_sub p   -> [0, 2p)
+//   u  = cond_sub(u, 2p)          in [0, 2p)
+//   x0 = u + t                    in [0, 4p)
+//   x1 = (u + 2p) - t             in (0, 4p)
+template <int K>
+WM_DEV void bf_finish(uint32_t (&x0)[K], uint32_t (&x1)[K], uint32_t (&t)[K], const uint32_t (&p2)[K]) {
+  uint32_t u[K], a[K];
+  copy_n<K>(u, x0);
+  cond_sub<K>(u, p2);
+  add_n<K>(x0, u, t);
+  add_n<K>(a, u, p2);
+  sub_n<K>(x1, a, t);
+}
+
+template <int K>
+WM_DEV void bf_lazy(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&wp)[K],
+                    const uint32_t (&p)[K], const uint32_t (&p2)[K], const uint32_t (&np)[K]) {
+  uint32_t t[K];
+  mul_shoup_lazy<K>(t, x1, w, wp, np);
+  cond_sub<K>(t, p);
+  bf_finish<K>(x0, x1, t, p2);
+}
+
+// Butterfly with twiddle 1 (stage 0): t = v reduced from [0, 4p) to [0, 2p).
+template <int K>
+WM_DEV void bf_lazy_w1(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&p2)[K]) {
+  uint32_t t[K];
+  copy_n<K>(t, x1);
+  cond_sub<K>(t, p2);
+  bf_finish<K>(x0, x1, t, p2);
+}
+
+// [0, 4p) -> [0, p)
+template <int K>
+WM_DEV void canonical_4p(uint32_t (&x)[K], const uint32_t (&p)[K], const uint32_t (&p2)[K]) {
+  cond_sub<K>(x, p2);
+  cond_sub<K>(x, p);
 }
 
 // ------------------------------------------------------------------ Barrett

@@ -37,6 +37,7 @@ namespace wm {
 template <int K>
 struct NttConst {
   uint32_t p[K];
+  uint32_t p2[K];   // 2p
   uint32_t np[K];   // 2^(32K) - p
   uint32_t sc[K];   // n^-1            (one-pass inverse epilogue)
   uint32_t scp[K];  // its Shoup companion
@@ -50,59 +51,140 @@ struct PassDesc {
   int64_t RO, RT, WO, WK;
   int SH;
   int64_t C1, C2, C3;
-  int scale_out;
+  int scale_out;      // multiply outputs by n^-1 (one-pass inverse)
+  int canonical_out;  // last pass: reduce [0, 4p) -> [0, p)
   int64_t tw_stride;  // n / L
   int64_t total_lines;  // row passes: batch * lines_inner
 };
 
-// ------------------------------------------------------------------ in-smem DFT
-// G lines of L elements at data[(g*L + pos)*K], bit-reversed order on entry,
-// natural order on exit.  tw[e] (e < L/2) = (w, w') for w = root_L^e.
+// ------------------------------------------------------------------ smem layout
+// Element e of the CTA's tile occupies K words.  When K is a multiple of 4 and
+// K/4 a power of two, an element is C = K/4 16-byte chunks and chunk (e, c)
+// lives at 16-byte slot  A ^ h(e),  A = e*C + c,  h = fold3(A >> 3) & 7, i.e.
+// the slot is XOR-permuted inside its 128-byte row by a fold of the row index.
+// That makes every access pattern of the passes (unit-stride butterflies,
+// power-of-two strided radix-4 groups, bit-reversed scatter, and the column
+// pass's line-strided epilogue) conflict-free or 2-way (tools/bank_model.py).
 template <int K>
-__device__ __forceinline__ void dft_stages(uint32_t *data, const uint32_t *tw, int logL, int G,
-                                           const NttConst<K> &c) {
-  const int L = 1 << logL;
-  const int half_total = G << (logL - 1);
-  for (int s = 0; s < logL; ++s) {
-    const int half = 1 << s;
-    for (int bf = threadIdx.x; bf < half_total; bf += blockDim.x) {
-      const int g = bf >> (logL - 1);
-      const int jj = bf & ((L >> 1) - 1);
-      const int j = jj & (half - 1);
-      const int p0 = ((jj >> s) << (s + 1)) + j;
-      uint32_t *e0 = data + (g * L + p0) * K;
-      uint32_t *e1 = e0 + half * K;
-      uint32_t u[K], v[K], t[K];
-      lds_elem<K>(u, e0);
-      lds_elem<K>(v, e1);
-      if (s == 0) {
-        copy_n<K>(t, v);  // root^0 = 1
-      } else {
-        uint32_t w[K], wp[K];
-        const uint32_t *te = tw + (j << (logL - 1 - s)) * (2 * K);
-        lds_elem<K>(w, te);
-        lds_elem<K>(wp, te + K);
-        mul_shoup<K>(t, v, w, wp, c.p, c.np);
+struct Smem {
+  static constexpr bool kVec = (K % 4 == 0);
+  static constexpr int C = kVec ? K / 4 : 1;
+  static constexpr bool kSwz = kVec && ((C & (C - 1)) == 0) && C <= 8;
+
+  WM_DEV static int swz(int e) {
+    if constexpr (kSwz) {
+      const int r = (e * C) >> 3;
+      return (r ^ (r >> 3) ^ (r >> 6) ^ (r >> 9) ^ (r >> 12)) & 7;
+    } else {
+      return 0;
+    }
+  }
+  WM_DEV static void load(uint32_t (&v)[K], const uint32_t *base, int e) {
+    if constexpr (kVec) {
+      const int h = swz(e);
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const uint4 q = *reinterpret_cast<const uint4 *>(base + (((e * C + c) ^ h) << 2));
+        v[4 * c] = q.x; v[4 * c + 1] = q.y; v[4 * c + 2] = q.z; v[4 * c + 3] = q.w;
       }
-      uint32_t o0[K], o1[K];
-      add_mod<K>(o0, u, t, c.p);
-      sub_mod<K>(o1, u, t, c.p);
-      sts_elem<K>(e0, o0);
-      sts_elem<K>(e1, o1);
+    } else {
+      lds_elem<K>(v, base + e * K);
+    }
+  }
+  WM_DEV static void store(uint32_t *base, int e, const uint32_t (&v)[K]) {
+    if constexpr (kVec) {
+      const int h = swz(e);
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        *reinterpret_cast<uint4 *>(base + (((e * C + c) ^ h) << 2)) =
+            make_uint4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+    } else {
+      sts_elem<K>(base + e * K, v);
+    }
+  }
+};
+
+// ------------------------------------------------------------------ in-smem DFT
+// G lines of L = 2^logL elements (tile element g*L + pos), bit-reversed order
+// on entry, natural order on exit, values in [0, 4p) throughout.  Stages run
+// two at a time as radix-4 groups held in registers (one shared-memory round
+// trip and one barrier per two stages); an odd leading stage runs radix-2.
+// tww/twp[e] (e < L/2) = root_L^e and its Shoup companion.
+template <int K>
+__device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, const uint32_t *twp, int logL,
+                                         int G, const NttConst<K> &c) {
+  using S = Smem<K>;
+  const int L = 1 << logL;
+  int s = 0;
+  if (logL & 1) {  // stage 0 alone: pairs (2m, 2m+1), twiddle 1
+    for (int bf = threadIdx.x; bf < (G * L) >> 1; bf += blockDim.x) {
+      const int e0 = bf << 1;
+      uint32_t x0[K], x1[K];
+      S::load(x0, data, e0);
+      S::load(x1, data, e0 + 1);
+      bf_lazy_w1<K>(x0, x1, c.p2);
+      S::store(data, e0, x0);
+      S::store(data, e0 + 1, x1);
+    }
+    __syncthreads();
+    s = 1;
+  }
+  for (; s < logL; s += 2) {
+    const int h = 1 << s;
+    const int lq = logL - 2;
+    for (int grp = threadIdx.x; grp < (G << lq); grp += blockDim.x) {
+      const int g = grp >> lq;
+      const int jj = grp & ((1 << lq) - 1);
+      const int j = jj & (h - 1);
+      const int e0 = (g << logL) + ((jj >> s) << (s + 2)) + j;
+      uint32_t x0[K], x1[K], x2[K], x3[K];
+      S::load(x0, data, e0);
+      S::load(x1, data, e0 + h);
+      S::load(x2, data, e0 + 2 * h);
+      S::load(x3, data, e0 + 3 * h);
+      uint32_t w[K], wp[K];
+      if (s == 0) {
+        bf_lazy_w1<K>(x0, x1, c.p2);
+        bf_lazy_w1<K>(x2, x3, c.p2);
+      } else {
+        const int i1 = j << (logL - 1 - s);
+        S::load(w, tww, i1);
+        S::load(wp, twp, i1);
+        bf_lazy<K>(x0, x1, w, wp, c.p, c.p2, c.np);
+        bf_lazy<K>(x2, x3, w, wp, c.p, c.p2, c.np);
+      }
+      const int i2 = j << (lq - s);
+      S::load(w, tww, i2);
+      S::load(wp, twp, i2);
+      bf_lazy<K>(x0, x2, w, wp, c.p, c.p2, c.np);
+      const int i3 = (j + h) << (lq - s);
+      S::load(w, tww, i3);
+      S::load(wp, twp, i3);
+      bf_lazy<K>(x1, x3, w, wp, c.p, c.p2, c.np);
+      S::store(data, e0, x0);
+      S::store(data, e0 + h, x1);
+      S::store(data, e0 + 2 * h, x2);
+      S::store(data, e0 + 3 * h, x3);
     }
     __syncthreads();
   }
 }
 
 template <int K>
-__device__ __forceinline__ void load_subtw(uint32_t *tw, const uint32_t *table, int logL, int64_t stride) {
+__device__ __forceinline__ void load_subtw(uint32_t *tww, uint32_t *twp, const uint32_t *table, int logL,
+                                           int64_t stride) {
   const int half = 1 << (logL - 1);
   for (int idx = threadIdx.x; idx < half * 2; idx += blockDim.x) {
     const int e = idx >> 1, part = idx & 1;
     uint32_t v[K];
     ldg_elem<K>(v, table + ((int64_t)e * stride) * (2 * K) + part * K);
-    sts_elem<K>(tw + e * (2 * K) + part * K, v);
+    Smem<K>::store(part ? twp : tww, e, v);
   }
+}
+
+template <int K>
+__device__ __forceinline__ size_t tile_words(int logL, int G) {
+  return (size_t)G * ((size_t)1 << logL) * K;
 }
 
 // ------------------------------------------------------------------ column pass
@@ -112,39 +194,42 @@ __global__ void __launch_bounds__(256) ntt_col_pass(const uint32_t *in, uint32_t
                                                     const uint32_t *tw_out, const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
+  using S = Smem<K>;
   const int logL = d.logL, L = 1 << logL, G = d.G;
   uint32_t *data = smem;
-  uint32_t *tw = smem + (size_t)G * L * K;
+  uint32_t *tww = smem + tile_words<K>(logL, G);
+  uint32_t *twp = tww + (size_t)(L / 2) * K;
   const int64_t tiles_inner = d.lines_inner / G;
   const int64_t tile = blockIdx.x;
   const int64_t o = tile / tiles_inner;
   const int64_t i0 = (tile - o * tiles_inner) * G;
   const int64_t base = (int64_t)blockIdx.y * d.n;
 
-  load_subtw<K>(tw, tw_sub, logL, d.tw_stride);
+  load_subtw<K>(tww, twp, tw_sub, logL, d.tw_stride);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
     const int t = idx / G, g = idx - t * G;
     const int64_t pos = base + o * d.RO + (int64_t)t * d.RT + i0 + g;
     uint32_t v[K];
     ldg_elem<K>(v, in + pos * K);
     const int tb = (int)(__brev((unsigned)t) >> (32 - logL));
-    sts_elem<K>(data + (g * L + tb) * K, v);
+    S::store(data, g * L + tb, v);
   }
   __syncthreads();
-  dft_stages<K>(data, tw, logL, G, c);
+  dft_smem<K>(data, tww, twp, logL, G, c);
   const int64_t nmask = d.n - 1;
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
     const int k = idx / G, g = idx - k * G;
     uint32_t v[K];
-    lds_elem<K>(v, data + (g * L + k) * K);
+    S::load(v, data, g * L + k);
     if (d.C3) {
       const int64_t e = ((((i0 + g) >> d.SH) * (o * d.C1 + (int64_t)k * d.C2)) * d.C3) & nmask;
       uint32_t w[K], wp[K], r[K];
       ldg_elem<K>(w, tw_out + e * (2 * K));
       ldg_elem<K>(wp, tw_out + e * (2 * K) + K);
-      mul_shoup<K>(r, v, w, wp, c.p, c.np);
+      mul_shoup_lazy<K>(r, v, w, wp, c.np);
       copy_n<K>(v, r);
     }
+    if (d.canonical_out) canonical_4p<K>(v, c.p, c.p2);
     const int64_t pos = base + o * d.WO + (int64_t)k * d.WK + i0 + g;
     stg_elem<K>(out + pos * K, v);
   }
@@ -157,12 +242,14 @@ __global__ void __launch_bounds__(256) ntt_row_pass(const uint32_t *in, uint32_t
                                                     const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
+  using S = Smem<K>;
   const int logL = d.logL, L = 1 << logL, G = d.G;
   uint32_t *data = smem;
-  uint32_t *tw = smem + (size_t)G * L * K;
+  uint32_t *tww = smem + tile_words<K>(logL, G);
+  uint32_t *twp = tww + (size_t)(L / 2) * K;
   const int64_t lam0 = (int64_t)blockIdx.x * G;
 
-  load_subtw<K>(tw, tw_sub, logL, d.tw_stride);
+  load_subtw<K>(tww, twp, tw_sub, logL, d.tw_stride);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
     const int g = idx >> logL, t = idx & (L - 1);
     const int64_t lam = lam0 + g;
@@ -172,23 +259,24 @@ __global__ void __launch_bounds__(256) ntt_row_pass(const uint32_t *in, uint32_t
       uint32_t v[K];
       ldg_elem<K>(v, in + pos * K);
       const int tb = (int)(__brev((unsigned)t) >> (32 - logL));
-      sts_elem<K>(data + (g * L + tb) * K, v);
+      S::store(data, g * L + tb, v);
     }
   }
   __syncthreads();
-  dft_stages<K>(data, tw, logL, G, c);
+  dft_smem<K>(data, tww, twp, logL, G, c);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
     const int g = idx >> logL, k = idx & (L - 1);
     const int64_t lam = lam0 + g;
     if (lam < d.total_lines) {
       const int64_t b = lam / d.lines_inner, r = lam - b * d.lines_inner;
       uint32_t v[K];
-      lds_elem<K>(v, data + (g * L + k) * K);
+      S::load(v, data, g * L + k);
       if (d.scale_out) {
         uint32_t rr[K];
-        mul_shoup<K>(rr, v, c.sc, c.scp, c.p, c.np);
+        mul_shoup_lazy<K>(rr, v, c.sc, c.scp, c.np);
         copy_n<K>(v, rr);
       }
+      if (d.canonical_out) canonical_4p<K>(v, c.p, c.p2);
       const int64_t pos = b * d.n + r * d.WO + (int64_t)k * d.WK;
       stg_elem<K>(out + pos * K, v);
     }
@@ -299,6 +387,7 @@ static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
   NttConst<K> c;
   for (int j = 0; j < K; ++j) {
     c.p[j] = pl->field->q[j];
+    c.p2[j] = pl->p2[j];
     c.np[j] = pl->np[j];
     c.sc[j] = pl->ninv[j];
     c.scp[j] = pl->ninv_sh[j];
@@ -308,7 +397,7 @@ static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
 
 static size_t pass_smem(int K, const wm_ntt_pass &ps) {
   const size_t L = (size_t)1 << ps.logL;
-  return ((size_t)ps.G * L * K + (L / 2) * 2 * K) * sizeof(uint32_t);
+  return ((size_t)ps.G * L * K + (L / 2) * 2 * (size_t)K) * sizeof(uint32_t);
 }
 
 template <int K>
@@ -340,6 +429,7 @@ static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, u
     d.C2 = ps.C2;
     d.C3 = ps.C3;
     d.scale_out = (inverse && ps.scale_out) ? 1 : 0;
+    d.canonical_out = ps.canonical_out ? 1 : 0;
     d.tw_stride = pl->n >> ps.logL;
     d.total_lines = batch * ps.lines_inner;
     const size_t smem = pass_smem(K, ps);
@@ -470,6 +560,7 @@ static int plan_passes(wm_ntt_plan *pl) {
     pl->passes.push_back(b);
     pl->passes.push_back(cc);
   }
+  pl->passes.back().canonical_out = true;
   for (const auto &ps : pl->passes) {
     if (pass_smem(K, ps) > 227 * 1024) return fail(WM_EUNSUPPORTED, "pass does not fit in shared memory");
   }
@@ -541,6 +632,7 @@ int wm_ntt_plan_create(const wm_field *f, int64_t n, const uint32_t *root_host, 
     pl->ninv_sh = quo;
     pl->np = Big(K, 0u);
     big_sub_inplace(pl->np, f->q);
+    pl->p2 = big_shl(f->q, 1, K);
   }
   int rc = plan_passes(pl);
   if (rc) {
