@@ -242,25 +242,19 @@ def run_gpu(args, rank, world, local, pg):
 
 
 def run_e2e(args, torch, dev, plan, field, ws, pg, world):
-    """Host (pinned) reference-layout buffers -> H2D -> layout convert ->
-    NTT -> INTT -> layout convert -> D2H, all inside the timed region."""
+    """Public API end to end: pinned HOST buffers in the reference layout
+    (AoS, 4 x 64-bit words MSW first per 256-bit value, kernels.to_words)
+    through the pipelined C ABI call wm_ntt_host (chunked H2D / layout
+    convert + NTT + INTT + convert / D2H on overlapping streams)."""
     host_in = torch.empty((BATCH * N, WORDS64), dtype=torch.int64, pin_memory=True)
     host_out = torch.empty_like(host_in)
     src = canonical_random(torch, BATCH * N, 99)
     host_in.copy_(field.to_ref_layout(src, 64, WORDS64).cpu())
-    d_ref = torch.empty((BATCH * N, WORDS64), dtype=torch.int64, device="cuda")
-    d_limbs = torch.empty((BATCH * N, K_LIMBS), dtype=torch.int32, device="cuda")
-    d_y = torch.empty_like(d_limbs)
-    d_out_ref = torch.empty_like(d_ref)
     stream = torch.cuda.current_stream()
 
     def step():
-        d_ref.copy_(host_in, non_blocking=True)
-        field.from_ref_layout(d_ref, 64, WORDS64, out=d_limbs)
-        plan.forward(d_limbs, out=d_y, workspace=ws)
-        plan.inverse(d_y, out=d_limbs, workspace=ws)
-        field.to_ref_layout(d_limbs, 64, WORDS64, out=d_out_ref)
-        host_out.copy_(d_out_ref, non_blocking=True)
+        plan.host_transform(host_in, host_out, mode="forward_inverse", word_bits=64, ref_words=WORDS64,
+                            chunk=args.e2e_chunk)
 
     for _ in range(max(1, args.warmup)):
         step()
@@ -278,7 +272,9 @@ def run_e2e(args, torch, dev, plan, field, ws, pg, world):
     nbytes = host_in.numel() * host_in.element_size()
     return {"value": ms * 1e3 / (world * args.steps * 2 * BATCH), "unit": UNIT,
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-            "path": "C ABI wm_ref_to_limbs + wm_ntt_forward + wm_ntt_inverse + wm_limbs_to_ref, pinned host buffers"}
+            "path": "NttPlan.host_transform -> C ABI wm_ntt_host(mode=FWD_INV): pinned host buffers, "
+                    "reference layout, chunked H2D/compute/D2H pipeline",
+            "chunk_transforms": args.e2e_chunk or "auto"}
 
 
 def run_blas(args, torch, _field, pg):
@@ -397,6 +393,7 @@ def main():
     ap.add_argument("--ref-transforms", type=int, default=32,
                     help="transforms per reference-arm step (a bounded sample of the 128)")
     ap.add_argument("--cpu-sample", type=int, default=16)
+    ap.add_argument("--e2e-chunk", type=int, default=0, help="transforms per host-pipeline chunk (0 = auto)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         log("note: warmup < 3 raised to 3")

@@ -130,6 +130,23 @@ int wm_ntt_inverse(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int6
 int wm_ntt_twiddles(const wm_ntt_plan *p, int inverse, int64_t count, uint32_t *out,
                     void *stream);
 
+/* ---------------------------------------------------------------- host pipeline
+ * End-to-end transforms on HOST buffers in the reference layout (AoS,
+ * `ref_words` words of `word_bits` bits per element, MSW first): the call a
+ * reference user makes with data in host memory.  The batch is processed in
+ * chunks of `chunk` transforms through a three-stage pipeline on the plan's
+ * internal streams — H2D copy, {layout convert, transform(s), layout convert},
+ * D2H copy — so PCIe traffic in both directions overlaps the kernels.  Host
+ * buffers should be pinned (cudaHostAlloc / cudaHostRegister) for overlap.
+ * mode: WM_NTT_FWD, WM_NTT_INV, or WM_NTT_FWD_INV (forward then inverse, the
+ * benchmark's round trip).  Ordered after prior work on `stream`; `stream`
+ * waits for the whole pipeline, so event timing on it brackets everything. */
+#define WM_NTT_FWD 0
+#define WM_NTT_INV 1
+#define WM_NTT_FWD_INV 2
+int wm_ntt_host(const wm_ntt_plan *p, int mode, int word_bits, int ref_words, const void *host_in,
+                void *host_out, int64_t batch, int64_t chunk, void *stream);
+
 /* ---------------------------------------------------------------- layout
  * Reference layout: AoS, `ref_words` words of `word_bits` (32 or 64) per
  * element, most-significant word first (kernels.to_words kernels.py:418-421;

@@ -18,6 +18,7 @@ WM_EINVAL = 1
 WM_ECUDA = 2
 WM_EUNSUPPORTED = 3
 WM_ELENGTH = 4
+WM_NTT_FWD, WM_NTT_INV, WM_NTT_FWD_INV = 0, 1, 2
 
 
 class LibraryUnavailable(RuntimeError):
@@ -60,6 +61,7 @@ SIGNATURES = [
     ("wm_ntt_forward", _int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     ("wm_ntt_inverse", _int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     ("wm_ntt_twiddles", _int, [_vp, _int, _i64, _vp, _vp]),
+    ("wm_ntt_host", _int, [_vp, _int, _int, _int, _vp, _vp, _i64, _i64, _vp]),
     ("wm_ref_to_limbs", _int, [_int, _int, _int, _vp, _vp, _i64, _vp]),
     ("wm_limbs_to_ref", _int, [_int, _int, _int, _vp, _vp, _i64, _vp]),
 ]

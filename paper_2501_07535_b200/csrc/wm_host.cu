@@ -1,0 +1,146 @@
+// Host-buffer pipeline (wm_ntt_host): the end-to-end path a reference user
+// takes — data in host memory in the reference's AoS MSW-first word layout
+// (kernels.to_words, kernels.py:418-428) — with PCIe traffic overlapped
+// against the kernels ("the host boundary's
+// throughput").
+//
+// Three plan-owned streams form a pipeline over chunks of `chunk` transforms
+// with kSlots staging slots in device memory:
+//   h2d stream:     wait slot free -> memcpy host_in chunk -> record ev_in
+//   compute stream: wait ev_in -> ref->limbs, NTT[/INTT], limbs->ref -> ev_comp
+//   d2h stream:     wait ev_comp -> memcpy to host_out -> record ev_out (slot free)
+// PCIe is full duplex, so the H2D of chunk c+1, the kernels of chunk c and the
+// D2H of chunk c-1 all run at once.
+#include <algorithm>
+
+#include "wm_internal.cuh"
+
+namespace wm {
+
+static int ensure_host_pipeline(wm_ntt_plan *p, int64_t slot_bytes) {
+  if (!p->host_ready) {
+    for (int i = 0; i < 3; ++i) WM_CUDA_TRY(cudaStreamCreateWithFlags(&p->hs[i], cudaStreamNonBlocking));
+    for (int s = 0; s < wm_ntt_plan::kSlots; ++s) {
+      WM_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_in[s], cudaEventDisableTiming));
+      WM_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_comp[s], cudaEventDisableTiming));
+      WM_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_out[s], cudaEventDisableTiming));
+    }
+    WM_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_entry, cudaEventDisableTiming));
+    WM_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+    p->host_ready = true;
+  }
+  if (p->slot_bytes < slot_bytes) {
+    for (int i = 0; i < 3; ++i) WM_CUDA_TRY(cudaStreamSynchronize(p->hs[i]));
+    for (int s = 0; s < wm_ntt_plan::kSlots; ++s) {
+      if (p->slot_mem[s]) WM_CUDA_TRY(cudaFree(p->slot_mem[s]));
+      p->slot_mem[s] = nullptr;
+    }
+    p->slot_bytes = 0;
+    for (int s = 0; s < wm_ntt_plan::kSlots; ++s) WM_CUDA_TRY(cudaMalloc(&p->slot_mem[s], slot_bytes));
+    p->slot_bytes = slot_bytes;
+  }
+  return WM_OK;
+}
+
+int release_host_pipeline(wm_ntt_plan *p) {
+  if (!p->host_ready) return WM_OK;
+  for (int i = 0; i < 3; ++i) {
+    cudaStreamSynchronize(p->hs[i]);
+    cudaStreamDestroy(p->hs[i]);
+  }
+  for (int s = 0; s < wm_ntt_plan::kSlots; ++s) {
+    cudaEventDestroy(p->ev_in[s]);
+    cudaEventDestroy(p->ev_comp[s]);
+    cudaEventDestroy(p->ev_out[s]);
+    if (p->slot_mem[s]) cudaFree(p->slot_mem[s]);
+  }
+  cudaEventDestroy(p->ev_entry);
+  cudaEventDestroy(p->ev_done);
+  p->host_ready = false;
+  return WM_OK;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+}  // namespace wm
+
+using namespace wm;
+
+extern "C" int wm_ntt_host(const wm_ntt_plan *pc, int mode, int word_bits, int ref_words, const void *host_in,
+                           void *host_out, int64_t batch, int64_t chunk, void *stream) {
+  if (!pc) return fail(WM_EINVAL, "null plan");
+  if (mode < WM_NTT_FWD || mode > WM_NTT_FWD_INV) return fail(WM_EINVAL, "bad mode");
+  if (word_bits != 32 && word_bits != 64) return fail(WM_EINVAL, "word_bits must be 32 or 64");
+  if ((int64_t)ref_words * word_bits < pc->field->bits) return fail(WM_EINVAL, "reference words too narrow");
+  if (batch < 0 || chunk < 0) return fail(WM_EINVAL, "negative batch/chunk");
+  if (batch == 0) return WM_OK;
+  if (!host_in || !host_out) return fail(WM_EINVAL, "null host pointer");
+  wm_ntt_plan *p = const_cast<wm_ntt_plan *>(pc);
+  const int64_t n = p->n;
+  const int K = p->K;
+  if (chunk == 0) chunk = std::max<int64_t>(1, (int64_t)(16 << 20) / (n * K * 4));  // ~16 MiB of limbs
+  chunk = std::min(chunk, batch);
+  const size_t ref_bytes_per_t = (size_t)n * ref_words * (word_bits / 8);
+  const size_t limb_bytes_per_t = (size_t)n * K * 4;
+  const size_t ref_sz = align256(ref_bytes_per_t * chunk);
+  const size_t limb_sz = align256(limb_bytes_per_t * chunk);
+  const size_t ws_sz = align256((size_t)std::max<int64_t>(0, wm_ntt_workspace_bytes(p, chunk)));
+  const size_t slot = ref_sz + 2 * limb_sz + ws_sz;
+
+  std::lock_guard<std::mutex> lk(p->host_mu);
+  int rc = ensure_host_pipeline(p, (int64_t)slot);
+  if (rc) return rc;
+  cudaStream_t user = (cudaStream_t)stream;
+  cudaStream_t h2d = p->hs[0], comp = p->hs[1], d2h = p->hs[2];
+  WM_CUDA_TRY(cudaEventRecord(p->ev_entry, user));
+  WM_CUDA_TRY(cudaStreamWaitEvent(h2d, p->ev_entry, 0));
+  WM_CUDA_TRY(cudaStreamWaitEvent(comp, p->ev_entry, 0));
+  WM_CUDA_TRY(cudaStreamWaitEvent(d2h, p->ev_entry, 0));
+
+  const int64_t nchunks = (batch + chunk - 1) / chunk;
+  for (int64_t c = 0; c < nchunks; ++c) {
+    const int s = (int)(c % wm_ntt_plan::kSlots);
+    const int64_t t0 = c * chunk;
+    const int64_t nt = std::min(chunk, batch - t0);
+    char *base = static_cast<char *>(p->slot_mem[s]);
+    void *d_ref = base;
+    uint32_t *d_a = reinterpret_cast<uint32_t *>(base + ref_sz);
+    uint32_t *d_b = reinterpret_cast<uint32_t *>(base + ref_sz + limb_sz);
+    void *d_ws = ws_sz ? base + ref_sz + 2 * limb_sz : nullptr;
+    const size_t rb = ref_bytes_per_t * nt;
+    if (c >= wm_ntt_plan::kSlots) WM_CUDA_TRY(cudaStreamWaitEvent(h2d, p->ev_out[s], 0));
+    WM_CUDA_TRY(cudaMemcpyAsync(d_ref, static_cast<const char *>(host_in) + ref_bytes_per_t * t0, rb,
+                                cudaMemcpyHostToDevice, h2d));
+    WM_CUDA_TRY(cudaEventRecord(p->ev_in[s], h2d));
+
+    WM_CUDA_TRY(cudaStreamWaitEvent(comp, p->ev_in[s], 0));
+    rc = wm_ref_to_limbs(word_bits, ref_words, K, d_ref, d_a, n * nt, comp);
+    if (rc) return rc;
+    uint32_t *res = d_a;
+    if (mode == WM_NTT_FWD || mode == WM_NTT_FWD_INV) {
+      rc = ntt_run_internal(p, false, d_a, d_b, nt, d_ws, comp);
+      if (rc) return rc;
+      res = d_b;
+    }
+    if (mode == WM_NTT_INV || mode == WM_NTT_FWD_INV) {
+      uint32_t *dst = (res == d_a) ? d_b : d_a;
+      rc = ntt_run_internal(p, true, res, dst, nt, d_ws, comp);
+      if (rc) return rc;
+      res = dst;
+    }
+    rc = wm_limbs_to_ref(word_bits, ref_words, K, res, d_ref, n * nt, comp);
+    if (rc) return rc;
+    WM_CUDA_TRY(cudaEventRecord(p->ev_comp[s], comp));
+
+    WM_CUDA_TRY(cudaStreamWaitEvent(d2h, p->ev_comp[s], 0));
+    WM_CUDA_TRY(cudaMemcpyAsync(static_cast<char *>(host_out) + ref_bytes_per_t * t0, d_ref, rb,
+                                cudaMemcpyDeviceToHost, d2h));
+    WM_CUDA_TRY(cudaEventRecord(p->ev_out[s], d2h));
+  }
+  WM_CUDA_TRY(cudaEventRecord(p->ev_done, d2h));
+  WM_CUDA_TRY(cudaStreamWaitEvent(user, p->ev_done, 0));
+  // keep the other internal streams ordered behind the finished pipeline
+  WM_CUDA_TRY(cudaStreamWaitEvent(h2d, p->ev_done, 0));
+  WM_CUDA_TRY(cudaStreamWaitEvent(comp, p->ev_done, 0));
+  return WM_OK;
+}

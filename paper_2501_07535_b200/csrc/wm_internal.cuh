@@ -91,4 +91,18 @@ struct wm_ntt_plan {
   std::mutex ws_mu;
   void *ws = nullptr;
   int64_t ws_bytes = 0;
+  // host pipeline (wm_ntt_host): internal streams, events and staging slots
+  std::mutex host_mu;
+  bool host_ready = false;
+  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
+  static constexpr int kSlots = 3;
+  cudaEvent_t ev_in[kSlots], ev_comp[kSlots], ev_out[kSlots], ev_entry = nullptr, ev_done = nullptr;
+  void *slot_mem[kSlots] = {nullptr, nullptr, nullptr};
+  int64_t slot_bytes = 0;
 };
+
+namespace wm {
+int ntt_run_internal(const wm_ntt_plan *p, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
+                     void *workspace, cudaStream_t st);
+int release_host_pipeline(wm_ntt_plan *p);
+}  // namespace wm

@@ -663,6 +663,7 @@ int wm_ntt_plan_destroy(wm_ntt_plan *p) {
   if (p->tw_inv) cudaFree(p->tw_inv);
   if (p->tw_inv_scaled) cudaFree(p->tw_inv_scaled);
   if (p->ws) cudaFree(p->ws);
+  release_host_pipeline(p);
   delete p;
   return WM_OK;
 }
@@ -680,8 +681,11 @@ int64_t wm_ntt_workspace_bytes(const wm_ntt_plan *p, int64_t batch) {
   return batch * p->n * p->K * (int64_t)sizeof(uint32_t);
 }
 
-static int ntt_run(const wm_ntt_plan *pc, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
-                   void *workspace, void *stream) {
+}  // extern "C"
+
+namespace wm {
+int ntt_run_internal(const wm_ntt_plan *pc, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
+                     void *workspace, cudaStream_t stream) {
   if (!pc) return fail(WM_EINVAL, "null plan");
   if (batch < 0) return fail(WM_EINVAL, "negative batch");
   if (batch == 0) return WM_OK;
@@ -715,6 +719,14 @@ static int ntt_run(const wm_ntt_plan *pc, bool inverse, const uint32_t *in, uint
     default:
       return fail(WM_EUNSUPPORTED, "limb count not built into the NTT kernels");
   }
+}
+}  // namespace wm
+
+extern "C" {
+
+static int ntt_run(const wm_ntt_plan *pc, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
+                   void *workspace, void *stream) {
+  return wm::ntt_run_internal(pc, inverse, in, out, batch, workspace, (cudaStream_t)stream);
 }
 
 int wm_ntt_forward(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int64_t batch, void *workspace,

@@ -255,6 +255,33 @@ class NttPlan:
         """x[j] = n^-1 sum_k y[k] root^(-jk) mod p per transform."""
         return self._run(self.lib.wm_ntt_inverse, x, out, workspace, stream)
 
+    def host_transform(self, host_in, host_out, mode: str = "forward", word_bits: int = 64,
+                       ref_words: int | None = None, chunk: int = 0, stream=None):
+        """End-to-end transform of HOST tensors in the reference layout (AoS,
+        MSW-first words, kernels.to_words) through the pipelined C ABI call
+        ``wm_ntt_host``: chunked H2D / kernels / D2H overlap.  mode is
+        "forward", "inverse" or "forward_inverse".  Pinned host tensors give
+        full PCIe overlap."""
+        codes = {"forward": _lib.WM_NTT_FWD, "inverse": _lib.WM_NTT_INV,
+                 "forward_inverse": _lib.WM_NTT_FWD_INV}
+        if mode not in codes:
+            raise ValueError(f"bad mode {mode!r}")
+        if ref_words is None:
+            ref_words = -(-self.field.bits // word_bits)
+            ref_words = 1 << (ref_words - 1).bit_length()  # reference pads to a power of two
+        if host_in.is_cuda or host_out.is_cuda:
+            raise ValueError("host_transform takes host tensors")
+        per = self.n * ref_words * word_bits // 8
+        nbytes = host_in.numel() * host_in.element_size()
+        if nbytes % per or host_out.numel() * host_out.element_size() != nbytes:
+            raise ValueError("host buffers are not a whole number of transforms")
+        if not (host_in.is_contiguous() and host_out.is_contiguous()):
+            raise ValueError("expected contiguous host tensors")
+        batch = nbytes // per
+        _lib.check(self.lib.wm_ntt_host(self._h, codes[mode], word_bits, ref_words, host_in.data_ptr(),
+                                        host_out.data_ptr(), batch, chunk, _stream_ptr(stream)), "wm_ntt_host")
+        return host_out
+
     def twiddles(self, count: int | None = None, inverse: bool = False, stream=None):
         """Device-generated powers root^e (root_inv^e), e < count."""
         torch = _torch()

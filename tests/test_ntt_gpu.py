@@ -182,3 +182,33 @@ def test_in_place_batch_and_workspace(cuda):
     assert np.array_equal(ref[n:2 * n], of.ntt(xl[n:2 * n], n, prm.root))
     with pytest.raises(ValueError):
         plan.forward(dev.to_device(xl[: n - 1]))
+
+
+@pytest.mark.parametrize("mode", ["forward", "inverse", "forward_inverse"])
+def test_host_pipeline_reference_layout(cuda, mode):
+    """wm_ntt_host: pinned host buffers in the reference AoS MSW-first layout
+    through the chunked H2D / kernels / D2H pipeline equal the device path."""
+    dev = _dev()
+    import torch
+    from paper_2501_07535_b200 import kernels as K
+    n, batch = 1 << 12, 7
+    plan = plan_for(256, n)
+    prm = plan.params
+    xs = bigint.uniform_residues(np.random.Generator(np.random.PCG64(31)), batch * n, prm.p)
+    ref_words = [w for v in xs for w in K.to_words(v, 4, 64)]
+    host_in = torch.from_numpy(np.array(ref_words, dtype=np.uint64).view(np.int64)).pin_memory()
+    host_out = torch.empty_like(host_in).pin_memory()
+    for chunk in (0, 1, 3, 7):
+        host_out.zero_()
+        plan.host_transform(host_in, host_out, mode=mode, word_bits=64, ref_words=4, chunk=chunk)
+        torch.cuda.synchronize()
+        words = host_out.numpy().view(np.uint64).tolist()
+        got = [K.from_words(words[i * 4:(i + 1) * 4], 64) for i in range(batch * n)]
+        xd = dev.to_device(dev.ints_to_limbs(xs, 8))
+        if mode == "forward":
+            want = plan.forward(xd)
+        elif mode == "inverse":
+            want = plan.inverse(xd)
+        else:
+            want = xd
+        assert got == dev.limbs_to_ints(dev.to_host(want)), chunk
