@@ -247,7 +247,7 @@ def run_e2e(args, torch, dev, plan, field, ws, pg, world):
     through the pipelined C ABI call wm_ntt_host (chunked H2D / layout
     convert + NTT + INTT + convert / D2H on overlapping streams)."""
     host_in = torch.empty((BATCH * N, WORDS64), dtype=torch.int64, pin_memory=True)
-    host_out = torch.empty_like(host_in)
+    host_out = torch.empty((BATCH * N, WORDS64), dtype=torch.int64, pin_memory=True)
     src = canonical_random(torch, BATCH * N, 99)
     host_in.copy_(field.to_ref_layout(src, 64, WORDS64).cpu())
     stream = torch.cuda.current_stream()

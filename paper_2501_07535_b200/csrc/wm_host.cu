@@ -78,7 +78,7 @@ extern "C" int wm_ntt_host(const wm_ntt_plan *pc, int mode, int word_bits, int r
   wm_ntt_plan *p = const_cast<wm_ntt_plan *>(pc);
   const int64_t n = p->n;
   const int K = p->K;
-  if (chunk == 0) chunk = std::max<int64_t>(1, (int64_t)(16 << 20) / (n * K * 4));  // ~16 MiB of limbs
+  if (chunk == 0) chunk = std::max<int64_t>(1, (int64_t)(8 << 20) / (n * K * 4));  // ~8 MiB of limbs (tools/e2e_probe.py)
   chunk = std::min(chunk, batch);
   const size_t ref_bytes_per_t = (size_t)n * ref_words * (word_bits / 8);
   const size_t limb_bytes_per_t = (size_t)n * K * 4;

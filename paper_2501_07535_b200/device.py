@@ -278,6 +278,10 @@ class NttPlan:
         if not (host_in.is_contiguous() and host_out.is_contiguous()):
             raise ValueError("expected contiguous host tensors")
         batch = nbytes // per
+        if not (host_in.is_pinned() and host_out.is_pinned()):
+            import warnings
+            warnings.warn("host_transform with pageable host memory: copies cannot overlap (pin the buffers)",
+                          RuntimeWarning, stacklevel=2)
         _lib.check(self.lib.wm_ntt_host(self._h, codes[mode], word_bits, ref_words, host_in.data_ptr(),
                                         host_out.data_ptr(), batch, chunk, _stream_ptr(stream)), "wm_ntt_host")
         return host_out

@@ -197,7 +197,7 @@ def test_host_pipeline_reference_layout(cuda, mode):
     xs = bigint.uniform_residues(np.random.Generator(np.random.PCG64(31)), batch * n, prm.p)
     ref_words = [w for v in xs for w in K.to_words(v, 4, 64)]
     host_in = torch.from_numpy(np.array(ref_words, dtype=np.uint64).view(np.int64)).pin_memory()
-    host_out = torch.empty_like(host_in).pin_memory()
+    host_out = torch.empty(host_in.shape, dtype=host_in.dtype, pin_memory=True)
     for chunk in (0, 1, 3, 7):
         host_out.zero_()
         plan.host_transform(host_in, host_out, mode=mode, word_bits=64, ref_words=4, chunk=chunk)
