@@ -147,6 +147,20 @@ int wm_ntt_twiddles(const wm_ntt_plan *p, int inverse, int64_t count, uint32_t *
 int wm_ntt_host(const wm_ntt_plan *p, int mode, int word_bits, int ref_words, const void *host_in,
                 void *host_out, int64_t batch, int64_t chunk, void *stream);
 
+/* ---------------------------------------------------------------- distributed four-step
+ * Pieces of the multi-GPU four-step NTT (one all-to-all per transform; the
+ * reference has no multi-GPU path).  See paper_2501_07535_b200/dist.py.
+ *   wm_transpose:        out[b][c][r] = in[b][r][c] for elements of `words` uint32s.
+ *   wm_scale_transpose:  out[c][r] = in[r][c] * table[r][c] mod p (canonical),
+ *                        table entries = (w, w') Shoup pairs of 2K words.
+ *   wm_twiddle_table_2d: table[r][c] = root^((row0 + r) * c mod n) as Shoup pairs. */
+int wm_transpose(int words, const uint32_t *in, uint32_t *out, int64_t rows, int64_t cols,
+                 int64_t batch, void *stream);
+int wm_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out,
+                       int64_t rows, int64_t cols, void *stream);
+int wm_twiddle_table_2d(const wm_field *f, int64_t n, const uint32_t *root_host, int64_t row0,
+                        int64_t rows, int64_t cols, uint32_t *table, void *stream);
+
 /* ---------------------------------------------------------------- layout
  * Reference layout: AoS, `ref_words` words of `word_bits` (32 or 64) per
  * element, most-significant word first (kernels.to_words kernels.py:418-421;

@@ -1,0 +1,238 @@
+// Device pieces of the distributed four-step NTT:
+// a single length-n transform split as n = N1 * N2 over P ranks with one
+// all-to-all.  With rank r holding rows j1 in its block (row j1 = x[j1 + N1 j2],
+// j2 = 0..N2-1), the forward transform is
+//   (a) N2-point row NTTs                  (wm_ntt_forward, batch N1/P)
+//   (b) Z[j1][k2] *= root^(j1 k2), transpose to [k2][j1]   (wm_scale_transpose)
+//   (c) all-to-all of the P column blocks  (NCCL, torch.distributed)
+//   (d) [P][N2/P][N1/P] -> [N2/P][P][N1/P] (wm_transpose on N1/P-element blocks)
+//   (e) N1-point row NTTs                  (wm_ntt_forward, batch N2/P)
+// leaving rank r with rows k2 in its block, row k2 = y[k2 + N2 k1].  The
+// reference has no multi-GPU path; the index algebra is the
+// four-step factorisation of ntt_reference's DFT (oracle.py:262-282).
+//
+// Both transposes are HBM-bound tile transposes through shared memory (32 x 32
+// elements per tile, coalesced on both sides); (b) fuses the twiddle multiply
+// (Shoup, canonical output) into the transpose so the twiddled data is written
+// once.
+#include <algorithm>
+
+#include "wm_internal.cuh"
+#include "wm_io.cuh"
+
+namespace wm {
+
+constexpr int TT = 32;  // tile edge (elements)
+
+// out[b][c][r] = in[b][r][c] for elements of W words.  Tile of TT x TT
+// elements staged in shared memory word-by-word (W words per element,
+// padded row stride to dodge bank conflicts).
+__global__ void __launch_bounds__(256) transpose_words_kernel(const uint32_t *in, uint32_t *out, int W,
+                                                              int64_t rows, int64_t cols) {
+  extern __shared__ uint32_t tile[];  // TT * (TT*W + 1) words
+  const int64_t b = blockIdx.z;
+  const int64_t r0 = (int64_t)blockIdx.y * TT, c0 = (int64_t)blockIdx.x * TT;
+  const int64_t plane = rows * cols * W;
+  const uint32_t *src = in + b * plane;
+  uint32_t *dst = out + b * plane;
+  const int stride = TT * W + 1;
+  // load: rows r0..r0+TT, each row a contiguous run of TT*W words
+  for (int idx = threadIdx.x; idx < TT * TT * W; idx += blockDim.x) {
+    const int rr = idx / (TT * W), w = idx - rr * (TT * W);
+    const int64_t r = r0 + rr, c = c0 + w / W;
+    if (r < rows && c < cols) tile[rr * stride + w] = src[(r * cols + c0) * W + w];
+  }
+  __syncthreads();
+  // store: out rows c0..c0+TT, each a contiguous run of TT*W words (elements r0..)
+  for (int idx = threadIdx.x; idx < TT * TT * W; idx += blockDim.x) {
+    const int cc = idx / (TT * W), w = idx - cc * (TT * W);
+    const int rr = w / W, ww = w - rr * W;
+    const int64_t c = c0 + cc, r = r0 + rr;
+    if (r < rows && c < cols) dst[(c * rows + r0) * W + w] = tile[rr * stride + cc * W + ww];
+  }
+}
+
+// out[c][r] = in[r][c] * table[r][c] (mod p), K-limb elements, canonical out.
+// table entries are (w, w') Shoup pairs (2K words).
+template <int K>
+__global__ void __launch_bounds__(256) scale_transpose_kernel(const uint32_t *in, const uint32_t *table,
+                                                              uint32_t *out, int64_t rows, int64_t cols,
+                                                              const __grid_constant__ FieldConst<K> F) {
+  extern __shared__ uint32_t tile[];  // TT * (TT*K + 1)
+  const int64_t r0 = (int64_t)blockIdx.y * TT, c0 = (int64_t)blockIdx.x * TT;
+  const int stride = TT * K + 1;
+  uint32_t np[K], p[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) p[j] = F.q[j];
+  // np = 2^(32K) - p
+  {
+    uint32_t z[K];
+    zero_n<K>(z);
+    sub_n<K>(np, z, p);
+  }
+  for (int idx = threadIdx.x; idx < TT * TT; idx += blockDim.x) {
+    const int rr = idx / TT, cc = idx - rr * TT;
+    const int64_t r = r0 + rr, c = c0 + cc;
+    if (r < rows && c < cols) {
+      uint32_t v[K], w[K], wp[K], res[K];
+      ldg_elem<K>(v, in + (r * cols + c) * K);
+      ldg_elem<K>(w, table + (r * cols + c) * (2 * K));
+      ldg_elem<K>(wp, table + (r * cols + c) * (2 * K) + K);
+      mul_shoup<K>(res, v, w, wp, p, np);
+#pragma unroll
+      for (int j = 0; j < K; ++j) tile[rr * stride + cc * K + j] = res[j];
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < TT * TT * K; idx += blockDim.x) {
+    const int cc = idx / (TT * K), w = idx - cc * (TT * K);
+    const int rr = w / K, ww = w - rr * K;
+    const int64_t c = c0 + cc, r = r0 + rr;
+    if (r < rows && c < cols) out[(c * rows + r0) * K + w] = tile[rr * stride + cc * K + ww];
+  }
+}
+
+// table[r][c] = (root^((row0 + r) * c mod n), companion), one thread per
+// chunk of a row: exponentiate once, then step by root^(row0 + r).
+template <int K>
+__global__ void twiddle_2d_kernel(uint32_t *table, int64_t n, int64_t row0, int64_t rows, int64_t cols,
+                                  int64_t chunk, const __grid_constant__ FieldConst<K> F,
+                                  const __grid_constant__ Limbs<K> root) {
+  const int64_t per_row = (cols + chunk - 1) / chunk;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= rows * per_row) return;
+  const int64_t r = t / per_row, c0 = (t - r * per_row) * chunk;
+  const int64_t c1 = (c0 + chunk < cols) ? c0 + chunk : cols;
+  const uint64_t j1 = (uint64_t)(row0 + r);
+  auto powmod = [&](uint32_t (&out)[K], uint64_t e) {
+    uint32_t b[K], tmp[K];
+    copy_n<K>(b, root.v);
+    zero_n<K>(out);
+    out[0] = 1;
+    for (; e; e >>= 1) {
+      if (e & 1) {
+        mul_barrett<K>(tmp, out, b, F);
+        copy_n<K>(out, tmp);
+      }
+      mul_barrett<K>(tmp, b, b, F);
+      copy_n<K>(b, tmp);
+    }
+  };
+  uint32_t x[K], step[K];
+  powmod(x, (j1 * (uint64_t)c0) & (uint64_t)(n - 1));
+  powmod(step, j1 & (uint64_t)(n - 1));
+  for (int64_t c = c0; c < c1; ++c) {
+    uint32_t wp[K], tmp[K];
+    shoup_companion_dev<K>(wp, x, F.q);
+    stg_elem<K>(table + (r * cols + c) * (2 * K), x);
+    stg_elem<K>(table + (r * cols + c) * (2 * K) + K, wp);
+    mul_barrett<K>(tmp, x, step, F);
+    copy_n<K>(x, tmp);
+  }
+}
+
+template <int K>
+static FieldConst<K> fconst(const wm_field *f) {
+  FieldConst<K> c;
+  for (int j = 0; j < K; ++j) {
+    c.q[j] = f->q[j];
+    c.qn[j] = f->qn[j];
+    c.qn2[j] = f->qn2[j];
+    c.nqn[j] = f->nqn[j];
+    c.mu8[j] = f->mu8[j];
+  }
+  c.s = (uint32_t)f->s;
+  return c;
+}
+
+template <int K>
+static int launch_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out,
+                                  int64_t rows, int64_t cols, cudaStream_t st) {
+  const size_t smem = (size_t)TT * (TT * K + 1) * 4;
+  static bool attr = false;
+  if (!attr) {
+    WM_CUDA_TRY(cudaFuncSetAttribute(scale_transpose_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smem, 48 * 1024)));
+    attr = true;
+  }
+  dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)((rows + TT - 1) / TT));
+  scale_transpose_kernel<K><<<grid, 256, smem, st>>>(in, table, out, rows, cols, fconst<K>(f));
+  WM_LAUNCH_CHECK("scale_transpose launch");
+  return WM_OK;
+}
+
+template <int K>
+static int launch_twiddle_2d(const wm_field *f, int64_t n, const uint32_t *root, int64_t row0, int64_t rows,
+                             int64_t cols, uint32_t *table, cudaStream_t st) {
+  Limbs<K> rt;
+  for (int j = 0; j < K; ++j) rt.v[j] = root[j];
+  const int64_t chunk = 64;
+  const int64_t threads = rows * ((cols + chunk - 1) / chunk);
+  const int grid = (int)((threads + 127) / 128);
+  twiddle_2d_kernel<K><<<grid, 128, 0, st>>>(table, n, row0, rows, cols, chunk, fconst<K>(f), rt);
+  WM_LAUNCH_CHECK("twiddle_2d launch");
+  return WM_OK;
+}
+
+}  // namespace wm
+
+using namespace wm;
+
+extern "C" {
+
+int wm_transpose(int words, const uint32_t *in, uint32_t *out, int64_t rows, int64_t cols, int64_t batch,
+                 void *stream) {
+  if (words < 1 || rows < 0 || cols < 0 || batch < 0) return fail(WM_EINVAL, "bad transpose shape");
+  if (rows == 0 || cols == 0 || batch == 0) return WM_OK;
+  if (!in || !out || in == out) return fail(WM_EINVAL, "transpose needs distinct in/out buffers");
+  const size_t smem = (size_t)TT * (TT * words + 1) * 4;
+  if (smem > 227 * 1024) return fail(WM_EUNSUPPORTED, "transpose element too wide");
+  static int attr_words = 0;
+  if (smem > 48 * 1024 && words > attr_words) {
+    WM_CUDA_TRY(cudaFuncSetAttribute(transpose_words_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    attr_words = words;
+  }
+  if (batch > 65535) return fail(WM_EUNSUPPORTED, "transpose batch above 65535");
+  dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)((rows + TT - 1) / TT), (unsigned)batch);
+  transpose_words_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(in, out, words, rows, cols);
+  WM_LAUNCH_CHECK("transpose launch");
+  return WM_OK;
+}
+
+int wm_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out, int64_t rows,
+                       int64_t cols, void *stream) {
+  if (!f) return fail(WM_EINVAL, "null field");
+  if (rows < 0 || cols < 0) return fail(WM_EINVAL, "bad shape");
+  if (rows == 0 || cols == 0) return WM_OK;
+  if (!in || !table || !out || in == out) return fail(WM_EINVAL, "bad pointers (in/out must differ)");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (f->K) {
+#define WM_CASE(k) \
+  case k:          \
+    return launch_scale_transpose<k>(f, in, table, out, rows, cols, st);
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      return fail(WM_EUNSUPPORTED, "limb count not built in");
+  }
+}
+
+int wm_twiddle_table_2d(const wm_field *f, int64_t n, const uint32_t *root_host, int64_t row0, int64_t rows,
+                        int64_t cols, uint32_t *table, void *stream) {
+  if (!f || !root_host || !table) return fail(WM_EINVAL, "null argument");
+  if (n < 1 || (n & (n - 1)) || rows < 0 || cols < 0 || row0 < 0) return fail(WM_EINVAL, "bad shape");
+  if (rows == 0 || cols == 0) return WM_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (f->K) {
+#define WM_CASE(k) \
+  case k:          \
+    return launch_twiddle_2d<k>(f, n, root_host, row0, rows, cols, table, st);
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      return fail(WM_EUNSUPPORTED, "limb count not built in");
+  }
+}
+
+}  // extern "C"

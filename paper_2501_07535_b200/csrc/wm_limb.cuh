@@ -303,6 +303,35 @@ WM_DEV void canonical_4p(uint32_t (&x)[K], const uint32_t (&p)[K], const uint32_
   cond_sub<K>(x, p);
 }
 
+// Fixed-size limb vector as a kernel parameter.
+template <int K>
+struct Limbs {
+  uint32_t v[K];
+};
+
+// wp = floor(w * 2^(32K) / p) by binary long division (w < p < 2^(32K-4)):
+// the Shoup companion of a fixed multiplier, computed on the device when
+// twiddle tables are generated (setup only, not on the hot path).
+template <int K>
+__device__ void shoup_companion_dev(uint32_t (&wp)[K], const uint32_t (&w)[K], const uint32_t (&p)[K]) {
+  uint32_t rem[K];
+  copy_n<K>(rem, w);
+#pragma unroll
+  for (int limb = K - 1; limb >= 0; --limb) {
+    uint32_t qw = 0;
+    for (int b = 31; b >= 0; --b) {
+      uint32_t sh[K], d[K];
+#pragma unroll
+      for (int j = K - 1; j > 0; --j) sh[j] = __funnelshift_l(rem[j - 1], rem[j], 1);
+      sh[0] = rem[0] << 1;
+      uint32_t br = sub_n<K>(d, sh, p);
+      select_n<K>(rem, br, sh, d);
+      qw = (qw << 1) | (br ? 0u : 1u);
+    }
+    wp[limb] = qw;
+  }
+}
+
 // ------------------------------------------------------------------ Barrett
 // Constants of a modulus q < 2^(32K-4) for the general multiply.  The modulus is
 // normalised to qn = q << s with 2^(M-1) <= qn < 2^M, M = 32K - 4, so that all

@@ -292,26 +292,6 @@ struct TwGenArgs {
   int64_t chunk;
 };
 
-// wp = floor(w * 2^(32K) / p) by binary long division (w < p < 2^(32K-4)).
-template <int K>
-__device__ void shoup_companion(uint32_t (&wp)[K], const uint32_t (&w)[K], const uint32_t (&p)[K]) {
-  uint32_t rem[K];
-  copy_n<K>(rem, w);
-#pragma unroll
-  for (int limb = K - 1; limb >= 0; --limb) {
-    uint32_t qw = 0;
-    for (int b = 31; b >= 0; --b) {
-      uint32_t sh[K];
-      shl_small<K>(sh, rem, 1u);
-      uint32_t d[K];
-      uint32_t br = sub_n<K>(d, sh, p);
-      select_n<K>(rem, br, sh, d);
-      qw = (qw << 1) | (br ? 0u : 1u);
-    }
-    wp[limb] = qw;
-  }
-}
-
 template <int K>
 __global__ void twiddle_gen_kernel(uint32_t *table, int64_t count, const __grid_constant__ TwGenArgs<K> a) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -332,7 +312,7 @@ __global__ void twiddle_gen_kernel(uint32_t *table, int64_t count, const __grid_
   const int64_t e1 = (e0 + a.chunk < count) ? e0 + a.chunk : count;
   for (int64_t e = e0; e < e1; ++e) {
     uint32_t wp[K];
-    shoup_companion<K>(wp, x, a.F.q);
+    shoup_companion_dev<K>(wp, x, a.F.q);
     stg_elem<K>(table + e * (2 * K), x);
     stg_elem<K>(table + e * (2 * K) + K, wp);
     uint32_t r[K];

@@ -1,0 +1,240 @@
+"""Multi-GPU partitioning of the hot path.
+
+* Batches of independent transforms and BLAS vectors shard by rank with no
+  collective at all (``shard_range``): every rank runs its own slice through
+  the single-GPU kernels; timing is max-over-ranks (bench.py).
+* A single long transform (config 5: 256-bit n = 2^24) is split four-step,
+  n = N1 * N2, over P ranks with exactly one all-to-all (``FourStepNtt``):
+
+      rank r holds rows j1 in its block (N1/P rows), row j1 = x[j1 + N1 j2]
+      (a) N2-point row NTTs                        wm_ntt_forward
+      (b) * root^(j1 k2), transpose to [k2][j1]    wm_scale_transpose (fused)
+      (c) all-to-all of the P column blocks        torch.distributed (NCCL)
+      (d) [P][N2/P][N1/P] -> [N2/P][N1]            wm_transpose (block transpose)
+      (e) N1-point row NTTs                        wm_ntt_forward
+      rank r now holds rows k2 in its block, row k2 = y[k2 + N2 k1]
+
+  The inverse runs the same five steps with the roles of N1 and N2 swapped
+  and inverse roots, mapping the output distribution back to the input one,
+  so INTT(NTT(x)) round-trips rank-locally.  The index algebra is the
+  four-step factorisation of the reference DFT y[k] = sum_j x[j] root^(jk)
+  (ntt_reference, oracle.py:262-282); the reference itself has no multi-GPU
+  path.
+
+The local compute is a *backend* object so the orchestration (block layout
+of the all-to-all, index maps) can be exercised on CPU with gloo in tests;
+the product backend is ``DeviceBackend`` (sm_100a kernels via the C ABI).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .params import NttParams
+
+
+def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous [start, stop) slice of `total` items for `rank` (weak or
+    strong scaling of batched transforms / BLAS vectors: no collective)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    base, extra = divmod(total, world)
+    start = rank * base + min(rank, extra)
+    return start, start + base + (1 if rank < extra else 0)
+
+
+def split_lengths(n: int) -> tuple[int, int]:
+    """n = N1 * N2 with N1 >= N2, both powers of two (N1 = 2^ceil(log n / 2))."""
+    if n < 4 or n & (n - 1):
+        raise ValueError("four-step needs a power-of-two length >= 4")
+    logn = n.bit_length() - 1
+    n1 = 1 << ((logn + 1) // 2)
+    return n1, n // n1
+
+
+@dataclass(frozen=True)
+class FourStepLayout:
+    """Index maps between the global vector and rank-local rows."""
+
+    n: int
+    n1: int
+    n2: int
+    world: int
+
+    def __post_init__(self):
+        if self.n1 * self.n2 != self.n:
+            raise ValueError("n != N1 * N2")
+        if self.n1 % self.world or self.n2 % self.world:
+            raise ValueError(f"world size {self.world} must divide N1={self.n1} and N2={self.n2}")
+
+    def input_rows(self, rank: int) -> range:
+        b = self.n1 // self.world
+        return range(rank * b, (rank + 1) * b)
+
+    def output_rows(self, rank: int) -> range:
+        b = self.n2 // self.world
+        return range(rank * b, (rank + 1) * b)
+
+    def scatter_input(self, x, rank: int):
+        """Global x[n] (array-like with a leading element axis) -> rank-local
+        [N1/P, N2, ...]: row j1 = x[j1 + N1*j2]."""
+        v = x.reshape((self.n2, self.n1) + tuple(x.shape[1:]))
+        r = self.input_rows(rank)
+        return _swap01(v[:, r.start:r.stop])
+
+    def gather_output(self, locals_):
+        """Rank-local outputs [N2/P, N1, ...] (rank order) -> global y[n]."""
+        import numpy as np
+        rows = np.concatenate([np.asarray(l) for l in locals_], axis=0)  # [N2, N1, ...]
+        return _swap01(rows).reshape((self.n,) + rows.shape[2:])
+
+    def scatter_output(self, y, rank: int):
+        v = y.reshape((self.n1, self.n2) + tuple(y.shape[1:]))
+        r = self.output_rows(rank)
+        return _swap01(v[:, r.start:r.stop])
+
+    def gather_input(self, locals_):
+        import numpy as np
+        rows = np.concatenate([np.asarray(l) for l in locals_], axis=0)  # [N1, N2, ...]
+        return _swap01(rows).reshape((self.n,) + rows.shape[2:])
+
+
+def _swap01(a):
+    import numpy as np
+    if isinstance(a, np.ndarray):
+        return np.ascontiguousarray(np.swapaxes(a, 0, 1))
+    return a.transpose(0, 1).contiguous()
+
+
+class TorchComm:
+    """all-to-all over a torch.distributed process group (NCCL on GPUs)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_to_all(self, out, inp):
+        self.dist.all_to_all_single(out.view(-1), inp.view(-1), group=self.group)
+        return out
+
+
+class DeviceBackend:
+    """Rank-local compute on the B200 (C ABI kernels)."""
+
+    def __init__(self, bits: int, params: NttParams, layout: FourStepLayout, rank: int):
+        import torch
+
+        from .device import Field, NttPlan, ints_to_limbs
+        from . import _lib
+        self.torch = torch
+        self.layout = layout
+        p, n = params.p, params.n
+        w, wi = params.root, params.root_inv
+        n1, n2, P = layout.n1, layout.n2, layout.world
+        self.field = Field(bits, p)
+        K = self.field.limbs
+        self.K = K
+
+        def sub_params(m: int, step: int) -> NttParams:
+            r = pow(w, step, p)
+            return NttParams(n=m, p=p, root=r, root_inv=pow(r, -1, p), n_inv=pow(m, -1, p))
+
+        self.plan_n2 = NttPlan(self.field, sub_params(n2, n1))  # root^(N1): order N2
+        self.plan_n1 = NttPlan(self.field, sub_params(n1, n2))  # root^(N2): order N1
+        lib = self.field.lib
+        enc = lambda v: _lib.u32_array(ints_to_limbs([v], K)[0].tolist())  # noqa: E731
+        stream = torch.cuda.current_stream().cuda_stream
+        rows_f, rows_i = n1 // P, n2 // P
+        self.tw_fwd = torch.empty((rows_f, n2, 2 * K), dtype=torch.int32, device="cuda")
+        _lib.check(lib.wm_twiddle_table_2d(self.field.handle, n, enc(w), rank * rows_f, rows_f, n2,
+                                           self.tw_fwd.data_ptr(), stream), "wm_twiddle_table_2d")
+        self.tw_inv = torch.empty((rows_i, n1, 2 * K), dtype=torch.int32, device="cuda")
+        _lib.check(lib.wm_twiddle_table_2d(self.field.handle, n, enc(wi), rank * rows_i, rows_i, n1,
+                                           self.tw_inv.data_ptr(), stream), "wm_twiddle_table_2d")
+        self.lib = lib
+        self._lib = _lib
+
+    def empty(self, shape):
+        return self.torch.empty(tuple(shape) + (self.K,), dtype=self.torch.int32, device="cuda")
+
+    def row_ntt(self, x, length: int, inverse: bool):
+        plan = self.plan_n2 if length == self.layout.n2 else self.plan_n1
+        return plan.inverse(x) if inverse else plan.forward(x)
+
+    def scale_transpose(self, x, inverse: bool):
+        rows, cols = x.shape[0], x.shape[1]
+        out = self.empty((cols, rows))
+        table = self.tw_inv if inverse else self.tw_fwd
+        stream = self.torch.cuda.current_stream().cuda_stream
+        self._lib.check(self.lib.wm_scale_transpose(self.field.handle, x.data_ptr(), table.data_ptr(),
+                                                    out.data_ptr(), rows, cols, stream), "wm_scale_transpose")
+        return out
+
+    def block_transpose(self, x, rows: int, cols: int, block: int):
+        """[rows][cols][block] -> [cols][rows][block] (block = elements)."""
+        out = self.empty((cols, rows * block))
+        stream = self.torch.cuda.current_stream().cuda_stream
+        self._lib.check(self.lib.wm_transpose(self.K * block, x.data_ptr(), out.data_ptr(), rows, cols, 1,
+                                              stream), "wm_transpose")
+        return out
+
+
+class FourStepNtt:
+    """One length-n NTT across the ranks of a communicator (see module doc)."""
+
+    def __init__(self, bits: int, params: NttParams, rank: int, world: int, backend=None, comm=None):
+        self.params = params
+        self.layout = FourStepLayout(params.n, *split_lengths(params.n), world)
+        self.rank, self.world = rank, world
+        self.backend = backend if backend is not None else DeviceBackend(bits, params, self.layout, rank)
+        self.comm = comm
+
+    # phase 1: local row transforms + twiddle/transpose -> send buffer
+    def phase1(self, x, inverse: bool):
+        L = self.layout
+        row_len = L.n1 if inverse else L.n2
+        y = self.backend.row_ntt(x, row_len, inverse)
+        return self.backend.scale_transpose(y, inverse)  # [row_len][rows_local]
+
+    # phase 2: received [P][row_len/P][rows_local] -> block transpose -> row transforms
+    def phase2(self, d, inverse: bool):
+        L = self.layout
+        P = self.world
+        row_len = L.n1 if inverse else L.n2      # length of the phase-1 rows
+        other = L.n2 if inverse else L.n1        # length of the phase-2 rows
+        rows_local = other // P
+        e = self.backend.block_transpose(d, P, row_len // P, rows_local)  # [row_len/P][other]
+        return self.backend.row_ntt(e, other, inverse)
+
+    def _run(self, x, inverse: bool):
+        c = self.phase1(x, inverse)
+        d = self.backend.empty(c.shape[:-1]) if hasattr(self.backend, "empty") else c.clone()
+        self.comm.all_to_all(d, c)
+        return self.phase2(d, inverse)
+
+    def forward(self, x):
+        """x: [N1/P, N2, K] local rows -> [N2/P, N1, K] (rows k2 of y)."""
+        return self._run(x, False)
+
+    def inverse(self, y):
+        """y: [N2/P, N1, K] -> [N1/P, N2, K] (rows j1 of x)."""
+        return self._run(y, True)
+
+
+def loopback_transform(engines, xs, inverse: bool = False):
+    """Run a FourStepNtt over P *virtual* ranks in one process (one engine per
+    virtual rank, typically all on one GPU): phase 1 on every rank, the
+    all-to-all as block copies, phase 2 on every rank.  Used to test the
+    distributed algorithm end to end on a single device."""
+    P = len(engines)
+    sends = [e.phase1(x, inverse) for e, x in zip(engines, xs)]
+    rows = sends[0].shape[0] // P  # send buffers are [row_len][rows_local]: P row blocks
+    recvs = []
+    for r in range(P):
+        parts = [s[r * rows:(r + 1) * rows] for s in sends]  # block r of every source, source order
+        import torch
+        recvs.append(torch.cat([p.reshape(-1) for p in parts]).reshape(sends[0].shape).contiguous())
+    return [e.phase2(d, inverse) for e, d in zip(engines, recvs)]

@@ -1,0 +1,104 @@
+"""The distributed four-step NTT on the B200: P virtual ranks on one GPU (the
+all-to-all as block copies, dist.loopback_transform) with the real device
+backend, checked against the single-GPU plan and the oracle; plus the
+transpose / twiddle-table kernels it is built from."""
+
+from __future__ import annotations
+
+import random
+
+import numpy as np
+import pytest
+
+from oracle.cbind import OracleField
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("logn,P", [(10, 1), (10, 2), (12, 4), (16, 2), (16, 8)])
+def test_loopback_four_step_matches_single_gpu(cuda, logn, P):
+    import torch
+    from paper_2501_07535_b200 import dist as D
+    from paper_2501_07535_b200 import kernels as K
+    from paper_2501_07535_b200.params import find_ntt_params
+    n = 1 << logn
+    prm = find_ntt_params(256, n)
+    engines = [D.FourStepNtt(256, prm, r, P) for r in range(P)]
+    L = engines[0].layout
+    g = torch.Generator(device="cuda").manual_seed(logn * 10 + P)
+    x = torch.randint(-(1 << 31), 1 << 31, (n, 8), dtype=torch.int32, device="cuda", generator=g)
+    x[:, 7] &= (1 << 27) - 1
+    xs = [L.scatter_input(x, r) for r in range(P)]
+    ys = D.loopback_transform(engines, xs)
+    y = L.gather_output([t.cpu().numpy() for t in ys])
+    want = K.get_plan(256, prm).forward(x).cpu().numpy()
+    assert np.array_equal(y, want)
+    back = D.loopback_transform(engines, ys, inverse=True)
+    for r in range(P):
+        assert torch.equal(back[r], xs[r])
+
+
+def test_transpose_kernel(cuda):
+    import torch
+    from paper_2501_07535_b200 import _lib
+    lib = _lib.load()
+    for words, rows, cols, batch in [(8, 33, 70, 2), (1, 1, 5, 1), (96, 8, 40, 1), (16, 64, 64, 3)]:
+        x = torch.randint(-(1 << 31), 1 << 31, (batch, rows, cols, words), dtype=torch.int32, device="cuda")
+        y = torch.empty((batch, cols, rows, words), dtype=torch.int32, device="cuda")
+        _lib.check(lib.wm_transpose(words, x.data_ptr(), y.data_ptr(), rows, cols, batch,
+                                    torch.cuda.current_stream().cuda_stream))
+        assert torch.equal(y, x.transpose(1, 2))
+
+
+def test_twiddle_table_and_scale_transpose(cuda):
+    import torch
+    from paper_2501_07535_b200 import _lib
+    from paper_2501_07535_b200 import device as dev
+    from paper_2501_07535_b200.params import find_ntt_params
+    lib = _lib.load()
+    n = 1 << 12
+    prm = find_ntt_params(256, n)
+    f = dev.Field(256, prm.p)
+    rows, cols, row0 = 20, 37, 100
+    tab = torch.empty((rows, cols, 16), dtype=torch.int32, device="cuda")
+    root = _lib.u32_array(dev.ints_to_limbs([prm.root], 8)[0].tolist())
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.wm_twiddle_table_2d(f.handle, n, root, row0, rows, cols, tab.data_ptr(), st))
+    got = dev.limbs_to_ints(dev.to_host(tab[..., :8].contiguous()).reshape(-1, 8))
+    want = [pow(prm.root, ((row0 + r) * c) % n, prm.p) for r in range(rows) for c in range(cols)]
+    assert got == want
+    comp = dev.limbs_to_ints(dev.to_host(tab[..., 8:].contiguous()).reshape(-1, 8))
+    assert comp == [(w << 256) // prm.p for w in want]
+    rnd = random.Random(1)
+    xs = [rnd.randrange(prm.p) for _ in range(rows * cols)]
+    x = dev.to_device(dev.ints_to_limbs(xs, 8)).reshape(rows, cols, 8)
+    out = torch.empty((cols, rows, 8), dtype=torch.int32, device="cuda")
+    _lib.check(lib.wm_scale_transpose(f.handle, x.data_ptr(), tab.data_ptr(), out.data_ptr(), rows, cols, st))
+    got = dev.limbs_to_ints(dev.to_host(out).reshape(-1, 8))
+    exp = [xs[r * cols + c] * want[r * cols + c] % prm.p for c in range(cols) for r in range(rows)]
+    assert got == exp
+
+
+def test_loopback_2p24_roundtrip_and_points(cuda):
+    """Config 5 size on one GPU as 2 virtual ranks: roundtrip and random
+    output points against the O(n) oracle."""
+    import torch
+    from paper_2501_07535_b200 import dist as D
+    from paper_2501_07535_b200.params import find_ntt_params
+    n, P = 1 << 24, 2
+    prm = find_ntt_params(256, n)
+    engines = [D.FourStepNtt(256, prm, r, P) for r in range(P)]
+    L = engines[0].layout
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.randint(-(1 << 31), 1 << 31, (n, 8), dtype=torch.int32, device="cuda", generator=g)
+    x[:, 7] &= (1 << 27) - 1
+    xs = [L.scatter_input(x, r) for r in range(P)]
+    ys = D.loopback_transform(engines, xs)
+    back = D.loopback_transform(engines, ys, inverse=True)
+    for r in range(P):
+        assert torch.equal(back[r], xs[r])
+    y = L.gather_output([t.cpu().numpy() for t in ys])
+    ks = [0, 5, n - 1] + [random.Random(3).randrange(n) for _ in range(3)]
+    pts = OracleField(prm.p, 256).ntt_points(x.cpu().numpy().view(np.uint32), prm.root, ks)
+    for i, k in enumerate(ks):
+        assert np.array_equal(y[k].view(np.uint32), pts[i])
