@@ -52,6 +52,23 @@ __global__ void __launch_bounds__(256) transpose_words_kernel(const uint32_t *in
   }
 }
 
+// Wide elements (>= 64 words, e.g. the N1/P-element blocks of the four-step's
+// block transpose): one CTA per element, 16-byte vector copies.
+__global__ void __launch_bounds__(256) transpose_wide_kernel(const uint32_t *in, uint32_t *out, int64_t W,
+                                                             int64_t rows, int64_t cols) {
+  const int64_t c = blockIdx.x, r = blockIdx.y, b = blockIdx.z;
+  const int64_t plane = rows * cols * W;
+  const uint32_t *src = in + b * plane + (r * cols + c) * W;
+  uint32_t *dst = out + b * plane + (c * rows + r) * W;
+  if ((W & 3) == 0) {
+    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+    for (int64_t i = threadIdx.x; i < W / 4; i += blockDim.x) d4[i] = __ldcs(s4 + i);
+  } else {
+    for (int64_t i = threadIdx.x; i < W; i += blockDim.x) dst[i] = src[i];
+  }
+}
+
 // out[c][r] = in[r][c] * table[r][c] (mod p), K-limb elements, canonical out.
 // table entries are (w, w') Shoup pairs (2K words).
 template <int K>
@@ -185,15 +202,20 @@ int wm_transpose(int words, const uint32_t *in, uint32_t *out, int64_t rows, int
   if (words < 1 || rows < 0 || cols < 0 || batch < 0) return fail(WM_EINVAL, "bad transpose shape");
   if (rows == 0 || cols == 0 || batch == 0) return WM_OK;
   if (!in || !out || in == out) return fail(WM_EINVAL, "transpose needs distinct in/out buffers");
+  if (batch > 65535 || rows > 65535) return fail(WM_EUNSUPPORTED, "transpose batch/rows above 65535");
+  if (words >= 64) {
+    dim3 g((unsigned)cols, (unsigned)rows, (unsigned)batch);
+    transpose_wide_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(in, out, words, rows, cols);
+    WM_LAUNCH_CHECK("transpose_wide launch");
+    return WM_OK;
+  }
   const size_t smem = (size_t)TT * (TT * words + 1) * 4;
-  if (smem > 227 * 1024) return fail(WM_EUNSUPPORTED, "transpose element too wide");
   static int attr_words = 0;
   if (smem > 48 * 1024 && words > attr_words) {
     WM_CUDA_TRY(cudaFuncSetAttribute(transpose_words_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
     attr_words = words;
   }
-  if (batch > 65535) return fail(WM_EUNSUPPORTED, "transpose batch above 65535");
   dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)((rows + TT - 1) / TT), (unsigned)batch);
   transpose_words_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(in, out, words, rows, cols);
   WM_LAUNCH_CHECK("transpose launch");
