@@ -226,8 +226,10 @@ def run_gpu(args, rank, world, local, pg):
     # ---- end-to-end through the C ABI with host buffers (reference layout)
     e2e = run_e2e(args, torch, dev, plan, field, ws, pg, world)
 
-    # ---- BLAS extra: 256-bit vmul n=2^24, HBM GB/s
-    blas = run_blas(args, torch, field, pg)
+    # ---- extras: BLAS sweep (configs[2]), four-step single 2^24 NTT (configs[4]), reference GPU code
+    blas = run_blas(args, torch, field, pg) if not args.skip_extras else None
+    four = run_four_step(args, torch, rank, world, pg) if not args.skip_extras else None
+    refgpu = run_reference_gpu(args, torch, plan) if (world == 1 and not args.skip_extras) else None
 
     return {
         "us_per_transform": us_per_transform,
@@ -238,6 +240,8 @@ def run_gpu(args, rank, world, local, pg):
         "clocks": clocks.summary(),
         "e2e": e2e,
         "blas": blas,
+        "four_step": four,
+        "reference_gpu": refgpu,
     }
 
 
@@ -278,31 +282,167 @@ def run_e2e(args, torch, dev, plan, field, ws, pg, world):
 
 
 def run_blas(args, torch, _field, pg):
+    """BASELINE configs[2]: vadd/vmul/axpy n=2^24 at 128/256/384/768 bits,
+    device-resident (inputs > L2), GB/s of algorithmic traffic (3 x 4K bytes
+    per element) vs the measured HBM copy bandwidth."""
     from paper_2501_07535_b200 import device as dev
     from paper_2501_07535_b200.params import find_ntt_params
     n = 1 << 24
+    hbm = peaks().get("hbm_gbs", 6650.0)
+    out_rows = []
+    stream = torch.cuda.current_stream()
+    for bits in args.blas_bits:
+        K = (bits + 31) // 32
+        q = find_ntt_params(bits, 1).p
+        f = dev.Field(bits, q)
+        g = torch.Generator(device="cuda").manual_seed(bits)
+        a = torch.randint(-(1 << 31), 1 << 31, (n, K), dtype=torch.int32, device="cuda", generator=g)
+        b = torch.randint(-(1 << 31), 1 << 31, (n, K), dtype=torch.int32, device="cuda", generator=g)
+        top = (1 << (bits - 5 - 32 * (K - 1))) - 1
+        a[:, K - 1] &= top
+        b[:, K - 1] &= top
+        out = torch.empty_like(a)
+        for op in ("vadd", "vmul", "axpy"):
+            fn = (lambda: f.axpy(123456789, a, b, out=out)) if op == "axpy" else \
+                (lambda op=op: getattr(f, op)(a, b, out=out))
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
+            for e0, e1 in evs:
+                e0.record(stream)
+                fn()
+                e1.record(stream)
+            torch.cuda.synchronize()
+            ms = statistics.median(x.elapsed_time(y) for x, y in evs)
+            gbs = 3 * 4 * K * n / (ms * 1e-3) / 1e9
+            out_rows.append({"op": op, "bits": bits, "n": n, "ms": round(ms, 4), "GB_per_s": round(gbs, 1),
+                             "hbm_frac_of_measured": round(gbs / hbm, 3)})
+        del a, b, out
+    return {"rows": out_rows, "hbm_measured_gbs": hbm,
+            "note": "median of 10 launches; operands 0.8-4.8 GB (> L2); bytes = 2 reads + 1 write per element"}
+
+
+def run_four_step(args, torch, rank, world, pg):
+    """BASELINE configs[4]: one 256-bit n=2^24 NTT split four-step over all
+    ranks with one NCCL all-to-all (at world=1: the same pipeline, no exchange)."""
+    from paper_2501_07535_b200 import dist as D
+    from paper_2501_07535_b200.params import find_ntt_params
+    n = 1 << 24
+    prm = find_ntt_params(BITS, n)
+    comm = D.TorchComm() if pg is not None else _SelfComm()
+    eng = D.FourStepNtt(BITS, prm, rank, world, comm=comm)
+    L = eng.layout
+    rows = L.n1 // world
+    x = canonical_random(torch, rows * L.n2, 4242 + rank).view(rows, L.n2, K_LIMBS)
+    for _ in range(2):
+        y = eng.forward(x)
+    torch.cuda.synchronize()
+    back = eng.inverse(y)
+    torch.cuda.synchronize()
+    assert torch.equal(back, x), "four-step roundtrip mismatch"
+    stream = torch.cuda.current_stream()
+    reps = 5
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(pg)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        eng.forward(x)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(pg, e0.elapsed_time(e1) / reps)
+    a2a_bytes = (world - 1) * (n // world) * 4 * K_LIMBS // world
+    return {"n": n, "ranks": world, "ms_per_forward": round(ms, 4), "us_per_transform": round(ms * 1e3, 2),
+            "split": [L.n1, L.n2], "a2a_bytes_sent_per_rank": a2a_bytes,
+            "note": "max over ranks; forward only; input rows j1 per rank (scatter not timed)"}
+
+
+class _SelfComm:
+    def all_to_all(self, out, inp):
+        out.copy_(inp)
+        return out
+
+
+def run_reference_gpu(args, torch, plan):
+    """The reference's own emit_cuda kernels compiled for sm_100a
+    (oracle/_ref/libref_gpu.so, built by oracle/gen_ref.py): vmul at 2^24 and
+    the NTT at the largest size that compiles (2^11, 256-bit), beside ours."""
+    path = ROOT / "oracle" / "_ref" / "libref_gpu.so"
+    if not path.exists():
+        return {"unavailable": "oracle/_ref/libref_gpu.so not built"}
+    from paper_2501_07535_b200 import device as dev
+    from paper_2501_07535_b200 import kernels as K
+    from paper_2501_07535_b200.params import find_ntt_params
+    lib = ctypes.CDLL(str(path))
+    vp, i = ctypes.c_void_p, ctypes.c_int
+    stream = torch.cuda.current_stream()
+    res = {}
+
+    def timed(fn, reps=10):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / reps
+
+    # vmul 2^24, reference layout (8 x 32-bit words, MSW first) == 32 B/element
+    n = 1 << 24
     q = find_ntt_params(BITS, 1).p
     f = dev.Field(BITS, q)
-    a = canonical_random(torch, n, 5)
-    b = canonical_random(torch, n, 6)
+    a = canonical_random(torch, n, 11)
+    b = canonical_random(torch, n, 12)
+    ra, rb = f.to_ref_layout(a, 32, 8), f.to_ref_layout(b, 32, 8)
+    rout = torch.empty_like(ra)
+    from paper_2501_07535_b200.params import compute_barrett
+    mu = compute_barrett(q, BITS).mu
+    muw = torch.tensor([w - (1 << 32) if w >= 1 << 31 else w for w in K.to_words(mu, 8, 32)],
+                       dtype=torch.int32).cuda()
+    qw = torch.tensor([w - (1 << 32) if w >= 1 << 31 else w for w in K.to_words(q, 8, 32)],
+                      dtype=torch.int32).cuda()
+    lib.vmul16777216_256w32_runtime_launch.argtypes = [vp, vp, vp, vp, vp, i]
+    lib.vmul16777216_256w32_baked_launch.argtypes = [vp, vp, vp, i]
+    ms_rt = timed(lambda: lib.vmul16777216_256w32_runtime_launch(ra.data_ptr(), rb.data_ptr(), qw.data_ptr(),
+                                                                  muw.data_ptr(), rout.data_ptr(), n))
+    ok_rt = torch.equal(f.from_ref_layout(rout, 32, 8), f.vmul(a, b))
+    ms_bk = timed(lambda: lib.vmul16777216_256w32_baked_launch(ra.data_ptr(), rb.data_ptr(), rout.data_ptr(), n))
+    ours = dev.Field(BITS, q)
     out = torch.empty_like(a)
-    for _ in range(3):
-        f.vmul(a, b, out=out)
+    ms_ours = timed(lambda: ours.vmul(a, b, out=out))
+    gb = 3 * 32 * n / 1e9
+    res["vmul_2p24"] = {"reference_runtime_q_GBps": round(gb / (ms_rt * 1e-3), 1),
+                        "reference_baked_q_GBps": round(gb / (ms_bk * 1e-3), 1),
+                        "ours_GBps": round(gb / (ms_ours * 1e-3), 1), "reference_matches_ours": bool(ok_rt),
+                        "speedup_vs_reference_runtime": round(ms_rt / ms_ours, 2)}
+    # NTT 2^11 (largest the reference's emitted CUDA compiles at 256 bits), batch 512
+    nn, batch = 1 << 11, 512
+    prm = find_ntt_params(BITS, nn)
+    pl = K.get_plan(BITS, prm)
+    x = canonical_random(torch, nn * batch, 13)
+    rx = pl.field.to_ref_layout(x, 32, 8)
+    ry = torch.empty_like(rx)
+    rz = torch.empty_like(rx)
+    lib.ntt2048_256w32_baked_launch.argtypes = [vp, vp, i]
+    lib.intt2048_256w32_baked_launch.argtypes = [vp, vp, i]
+    ms_ref = timed(lambda: (lib.ntt2048_256w32_baked_launch(rx.data_ptr(), ry.data_ptr(), batch),
+                            lib.intt2048_256w32_baked_launch(ry.data_ptr(), rz.data_ptr(), batch)), reps=3)
+    lib.ntt2048_256w32_baked_launch(rx.data_ptr(), ry.data_ptr(), batch)
     torch.cuda.synchronize()
-    reps = 10
-    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
-    stream = torch.cuda.current_stream()
-    for s in range(reps):
-        evs[s][0].record(stream)
-        f.vmul(a, b, out=out)
-        evs[s][1].record(stream)
-    torch.cuda.synchronize()
-    ms = statistics.median(x.elapsed_time(y) for x, y in evs)
-    gbs = 3 * 32 * n / (ms * 1e-3) / 1e9
-    hbm = peaks().get("hbm_gbs", 6650.0)
-    return {"op": "vmul", "bits": BITS, "n": n, "ms": ms, "GB_per_s": gbs,
-            "hbm_frac_of_measured": gbs / hbm, "hbm_measured_gbs": hbm,
-            "note": "inputs 1.5 GiB > L2; median of 10"}
+    ok = torch.equal(pl.field.from_ref_layout(ry, 32, 8), pl.forward(x))
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    ms_us = timed(lambda: (pl.forward(x, out=y), pl.inverse(y, out=z)))
+    res["ntt_2p11"] = {"batch": batch, "reference_us_per_transform": round(ms_ref * 1e3 / (2 * batch), 3),
+                       "ours_us_per_transform": round(ms_us * 1e3 / (2 * batch), 4),
+                       "speedup": round(ms_ref / ms_us, 1), "reference_matches_ours": bool(ok),
+                       "note": "reference emit_cuda: bit-reverse + one launch per stage, __constant__ twiddles; "
+                               "n >= 2^12 does not compile (constant bank overflow)"}
+    return res
 
 
 # ------------------------------------------------------------ CPU baselines
@@ -393,6 +533,8 @@ def main():
     ap.add_argument("--ref-transforms", type=int, default=32,
                     help="transforms per reference-arm step (a bounded sample of the 128)")
     ap.add_argument("--cpu-sample", type=int, default=16)
+    ap.add_argument("--skip-extras", action="store_true", help="only the headline workload")
+    ap.add_argument("--blas-bits", type=int, nargs="*", default=[128, 256, 384, 768])
     ap.add_argument("--e2e-chunk", type=int, default=0, help="transforms per host-pipeline chunk (0 = auto)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
@@ -461,6 +603,8 @@ def main():
         "cpu_baseline": cpu,
         "clocks": res["clocks"],
         "blas": res["blas"],
+        "four_step_2p24": res["four_step"],
+        "reference_gpu": res["reference_gpu"],
     }
     print(json.dumps(out))
     if pg is not None:

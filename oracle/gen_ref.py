@@ -23,6 +23,12 @@ HERE = Path(__file__).resolve().parent
 OUT = HERE / "_ref"
 REF_SRC = Path("/root/reference/pkg/src")
 
+# reference GPU kernels (emit_cuda text compiled for sm_100a): (kind, bits, word, size, params_mode).
+# The NTT is the largest size whose __constant__ twiddle table still fits (2^11 at 256 bits).
+GPU_KERNELS = [("vmul", 256, 32, 1 << 24, "runtime"), ("vmul", 256, 32, 1 << 24, "baked"),
+               ("vadd", 256, 32, 1 << 24, "baked"), ("ntt", 256, 32, 1 << 11, "baked"),
+               ("intt", 256, 32, 1 << 11, "baked")]
+
 # (kind, bits, word, size): the bench workload's transforms and the BLAS sweep
 NTT_KERNELS = [("ntt", 256, 64, 1 << 16), ("intt", 256, 64, 1 << 16)]
 BLAS_KERNELS = [(k, b, 64, 1) for b in (128, 256, 384, 768) for k in ("vadd", "vmul", "axpy")]
@@ -90,9 +96,39 @@ def main() -> int:
     subprocess.run(["gcc", "-shared", "-fopenmp", "-o", str(lib), *objs], check=True)
     for o in objs:
         os.remove(o)
+    build_gpu(emit_cuda_fn=None)
     (OUT / "MANIFEST").write_text("\n".join(f"{k} {b} {w} {s}" for k, b, w, s in NTT_KERNELS + BLAS_KERNELS) + "\n")
     print(f"gen_ref: built {lib}")
     return 0
+
+
+def build_gpu(emit_cuda_fn=None) -> None:
+    """The reference's own emitted CUDA (emit.emit_cuda, emit.py:414-561),
+    compiled for sm_100a into oracle/_ref/libref_gpu.so: the reference GPU
+    baseline (one thread per element / one launch per NTT stage)."""
+    import shutil
+    from widemod.emit import emit_cuda
+    from widemod.kernels import generate_kernel, make_spec
+    nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
+    objs = []
+    for kind, bits, word, size, mode in GPU_KERNELS:
+        prog = generate_kernel(make_spec(kind, bits, word, size=size), params_mode=mode)
+        src = emit_cuda(prog)
+        name = f"{prog.name}_{mode}"
+        # every symbol carries the program name; make the two params modes distinct
+        src = src.replace(prog.name, name)
+        f = OUT / f"{name}.emitted.cu"
+        f.write_text(src)
+        o = f.with_suffix(".o")
+        subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-Xcompiler", "-fPIC",
+                        "-c", str(f), "-o", str(o)], check=True)
+        objs.append(str(o))
+        print(f"gen_ref: compiled reference CUDA {name}", flush=True)
+    lib = OUT / "libref_gpu.so"
+    subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(lib), *objs],
+                   check=True)
+    for o in objs:
+        os.remove(o)
 
 
 if __name__ == "__main__":
