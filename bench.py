@@ -406,18 +406,31 @@ def run_reference_gpu(args, torch, plan):
     qw = torch.tensor([w - (1 << 32) if w >= 1 << 31 else w for w in K.to_words(q, 8, 32)],
                       dtype=torch.int32).cuda()
     lib.vmul16777216_256w32_runtime_launch.argtypes = [vp, vp, vp, vp, vp, i]
-    lib.vmul16777216_256w32_baked_launch.argtypes = [vp, vp, vp, i]
-    ms_rt = timed(lambda: lib.vmul16777216_256w32_runtime_launch(ra.data_ptr(), rb.data_ptr(), qw.data_ptr(),
-                                                                  muw.data_ptr(), rout.data_ptr(), n))
+    lib.refdrv_vmul16777216_256w32_runtime.argtypes = [vp, vp, vp, vp, vp, i, i]
+    lib.refdrv_vmul16777216_256w32_baked.argtypes = [vp, vp, vp, i, i]
+    # the reference's own launcher (1024 threads/block): does it launch at all?
+    rout.zero_()
+    torch.cuda.synchronize()
+    lib.vmul16777216_256w32_runtime_launch(ra.data_ptr(), rb.data_ptr(), qw.data_ptr(), muw.data_ptr(),
+                                           rout.data_ptr(), n)
+    torch.cuda.synchronize()
+    launch_err = "kernel did not run (output untouched)" if not bool(rout.any()) else "ran"
+    thr = 256
+    ms_rt = timed(lambda: lib.refdrv_vmul16777216_256w32_runtime(ra.data_ptr(), rb.data_ptr(), qw.data_ptr(),
+                                                                  muw.data_ptr(), rout.data_ptr(), n, thr))
     ok_rt = torch.equal(f.from_ref_layout(rout, 32, 8), f.vmul(a, b))
-    ms_bk = timed(lambda: lib.vmul16777216_256w32_baked_launch(ra.data_ptr(), rb.data_ptr(), rout.data_ptr(), n))
+    ms_bk = timed(lambda: lib.refdrv_vmul16777216_256w32_baked(ra.data_ptr(), rb.data_ptr(), rout.data_ptr(), n,
+                                                               thr))
+    ok_bk = torch.equal(f.from_ref_layout(rout, 32, 8), f.vmul(a, b))
     ours = dev.Field(BITS, q)
     out = torch.empty_like(a)
     ms_ours = timed(lambda: ours.vmul(a, b, out=out))
     gb = 3 * 32 * n / 1e9
     res["vmul_2p24"] = {"reference_runtime_q_GBps": round(gb / (ms_rt * 1e-3), 1),
                         "reference_baked_q_GBps": round(gb / (ms_bk * 1e-3), 1),
-                        "ours_GBps": round(gb / (ms_ours * 1e-3), 1), "reference_matches_ours": bool(ok_rt),
+                        "ours_GBps": round(gb / (ms_ours * 1e-3), 1),
+                        "reference_matches_ours": bool(ok_rt and ok_bk),
+                        "reference_launcher_1024_threads_error": str(launch_err),
                         "speedup_vs_reference_runtime": round(ms_rt / ms_ours, 2)}
     # NTT 2^11 (largest the reference's emitted CUDA compiles at 256 bits), batch 512
     nn, batch = 1 << 11, 512
@@ -427,11 +440,11 @@ def run_reference_gpu(args, torch, plan):
     rx = pl.field.to_ref_layout(x, 32, 8)
     ry = torch.empty_like(rx)
     rz = torch.empty_like(rx)
-    lib.ntt2048_256w32_baked_launch.argtypes = [vp, vp, i]
-    lib.intt2048_256w32_baked_launch.argtypes = [vp, vp, i]
-    ms_ref = timed(lambda: (lib.ntt2048_256w32_baked_launch(rx.data_ptr(), ry.data_ptr(), batch),
-                            lib.intt2048_256w32_baked_launch(ry.data_ptr(), rz.data_ptr(), batch)), reps=3)
-    lib.ntt2048_256w32_baked_launch(rx.data_ptr(), ry.data_ptr(), batch)
+    lib.refdrv_ntt2048_256w32_baked.argtypes = [vp, vp, i, i]
+    lib.refdrv_intt2048_256w32_baked.argtypes = [vp, vp, i, i]
+    ms_ref = timed(lambda: (lib.refdrv_ntt2048_256w32_baked(rx.data_ptr(), ry.data_ptr(), batch, thr),
+                            lib.refdrv_intt2048_256w32_baked(ry.data_ptr(), rz.data_ptr(), batch, thr)), reps=3)
+    lib.refdrv_ntt2048_256w32_baked(rx.data_ptr(), ry.data_ptr(), batch, thr)
     torch.cuda.synchronize()
     ok = torch.equal(pl.field.from_ref_layout(ry, 32, 8), pl.forward(x))
     y = torch.empty_like(x)
@@ -440,8 +453,9 @@ def run_reference_gpu(args, torch, plan):
     res["ntt_2p11"] = {"batch": batch, "reference_us_per_transform": round(ms_ref * 1e3 / (2 * batch), 3),
                        "ours_us_per_transform": round(ms_us * 1e3 / (2 * batch), 4),
                        "speedup": round(ms_ref / ms_us, 1), "reference_matches_ours": bool(ok),
-                       "note": "reference emit_cuda: bit-reverse + one launch per stage, __constant__ twiddles; "
-                               "n >= 2^12 does not compile (constant bank overflow)"}
+                       "note": "reference emit_cuda kernels (bit-reverse + one launch per stage, __constant__ "
+                               "twiddles) driven at 256 threads/block: its own launcher's 1024 threads/block cannot "
+                               "launch at 256 bits; n >= 2^12 does not compile (constant bank overflow)"}
     return res
 
 

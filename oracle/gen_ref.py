@@ -102,6 +102,27 @@ def main() -> int:
     return 0
 
 
+def _gpu_driver(prog, name: str, kind: str, size: int) -> str:
+    attrs = prog.attributes
+    args = attrs["arg_names"]
+    if kind in ("ntt", "intt"):
+        n = size
+        stages = n.bit_length() - 1
+        lines = [f'extern "C" int refdrv_{name}(const w32 *in, w32 *x, int batch, int threads) {{',
+                 f"    dim3 gf(({n} + threads - 1) / threads, batch), gh(({n // 2} + threads - 1) / threads, batch);",
+                 f"    {name}_bitrev<<<gf, threads>>>(in, x);"]
+        lines += [f"    {name}_stage{s}<<<gh, threads>>>(x);" for s in range(stages)]
+        if kind == "intt":
+            lines.append(f"    {name}_scale<<<gf, threads>>>(x);")
+        lines += ["    return (int)cudaGetLastError();", "}"]
+        return "\n" + "\n".join(lines) + "\n"
+    params = ", ".join(f"const w32 *{a}" for a in args) + ", w32 *out, int n_elems, int threads"
+    call = ", ".join(list(args) + ["out", "n_elems"])
+    return (f'\nextern "C" int refdrv_{name}({params}) {{\n'
+            f"    {name}_kernel<<<(n_elems + threads - 1) / threads, threads>>>({call});\n"
+            f"    return (int)cudaGetLastError();\n}}\n")
+
+
 def build_gpu(emit_cuda_fn=None) -> None:
     """The reference's own emitted CUDA (emit.emit_cuda, emit.py:414-561),
     compiled for sm_100a into oracle/_ref/libref_gpu.so: the reference GPU
@@ -117,6 +138,12 @@ def build_gpu(emit_cuda_fn=None) -> None:
         name = f"{prog.name}_{mode}"
         # every symbol carries the program name; make the two params modes distinct
         src = src.replace(prog.name, name)
+        # The emitted launcher hard-codes min(n, 1024) threads per block, which
+        # cannot launch on B200 once the straight-line body needs > 64
+        # registers (256-bit: it fails silently -- the reference launcher has
+        # no error channel).  Add our own driver that runs the SAME emitted
+        # kernels in the SAME order with a launchable block size.
+        src += _gpu_driver(prog, name, kind, size)
         f = OUT / f"{name}.emitted.cu"
         f.write_text(src)
         o = f.with_suffix(".o")
