@@ -48,20 +48,25 @@ def _digest() -> str:
     return h.hexdigest()
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    """Compile the library if sources changed; return its path."""
-    stamp = PKG / ".libwidemod_b200.stamp"
-    digest = _digest()
-    if (not force and LIB_PATH.exists() and stamp.exists()
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines: tuple[str, ...] = ()) -> Path:
+    """Compile the library if sources changed; return its path.  A `variant`
+    (with extra -D `defines`) builds an experimental copy
+    libwidemod_b200_<variant>.so next to the main one (A/B timing only)."""
+    lib_path = LIB_PATH if variant is None else PKG / f"libwidemod_b200_{variant}.so"
+    stamp = PKG / (".libwidemod_b200.stamp" if variant is None else f".libwidemod_b200_{variant}.stamp")
+    digest = _digest() + ",".join(defines)
+    if (not force and lib_path.exists() and stamp.exists()
             and stamp.read_text().strip() == digest):
-        return LIB_PATH
+        return lib_path
     nvcc = _nvcc()
-    objdir = PKG / "build"
-    objdir.mkdir(exist_ok=True)
+    objdir = PKG / "build" / (variant or "main")
+    objdir.mkdir(parents=True, exist_ok=True)
+    dflags = [f"-D{d}" for d in defines]
 
     def compile_one(src: Path) -> Path:
         obj = objdir / (src.stem + ".o")
-        cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+        cmd = [nvcc, *ARCH_FLAGS, *NVCC_FLAGS, *dflags, "-c", str(src), "-o", str(obj)]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src.name}:\n{res.stderr}")
@@ -71,14 +76,14 @@ def build(force: bool = False, verbose: bool = False) -> Path:
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         objs = list(ex.map(compile_one, _sources()))
-    tmp = LIB_PATH.with_suffix(".so.tmp")
+    tmp = lib_path.with_suffix(".so.tmp")
     cmd = [nvcc, *ARCH_FLAGS, "-shared", "-o", str(tmp), *map(str, objs)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed:\n{res.stderr}")
-    os.replace(tmp, LIB_PATH)
+    os.replace(tmp, lib_path)
     stamp.write_text(digest)
-    return LIB_PATH
+    return lib_path
 
 
 if __name__ == "__main__":

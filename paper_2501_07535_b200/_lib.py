@@ -76,7 +76,9 @@ def load(path: str | Path | None = None, build_if_missing: bool = True):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        import os
+        env = os.environ.get("WM_LIB_PATH")  # A/B experiments only (tools/ab_timing.py)
+        p = Path(path) if path else (Path(env) if env else LIB_PATH)
         if not p.exists():
             if not build_if_missing:
                 raise LibraryUnavailable(f"{p} not built")

@@ -151,7 +151,7 @@ WM_DEV void mac_row(uint32_t (&acc)[N], const int base, const uint32_t (&a)[K], 
 
 // t = a * b, full 2K-limb product (schoolbook, row scanning).  K^2 IMAD.WIDE.
 template <int K>
-WM_DEV void mul_full(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+WM_DEV void mul_full_ptx(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
 #pragma unroll
   for (int j = 0; j < 2 * K; ++j) t[j] = 0u;
 #pragma unroll
@@ -163,7 +163,7 @@ WM_DEV void mul_full(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_
 // carries are dropped).  The neglected sum is < C0 * 2^(32(C0+1)) < 2^(32K-27),
 // so the result is the exact high half or one less.  K^2 - (K-2)(K-1)/2 products.
 template <int K>
-WM_DEV void mul_hi_trunc(uint32_t (&h)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+WM_DEV void mul_hi_trunc_ptx(uint32_t (&h)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
   constexpr int C0 = (K > 2) ? K - 2 : 0;
   constexpr int W = 2 * K - C0;  // columns C0 .. 2K-1, acc[c - C0]
   uint32_t acc[W + 1];
@@ -205,7 +205,7 @@ WM_DEV void mul_hi_trunc(uint32_t (&h)[K], const uint32_t (&a)[K], const uint32_
 // r += a * b (mod 2^(32K)): only the partial products that land in the low K
 // limbs.  K(K-1)/2 IMAD.WIDE + K plain IMAD (the top column's low halves).
 template <int K>
-WM_DEV void mul_lo_acc(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+WM_DEV void mul_lo_acc_ptx(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     const int m = K - i;  // a_0 .. a_{m-1} reach limbs i .. K-1
@@ -234,6 +234,83 @@ WM_DEV void mul_lo_acc(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t 
     }
   }
 }
+
+// t = a * b, full 2K-limb product (schoolbook, row scanning).  K^2 IMAD.WIDE.
+template <int K>
+WM_DEV void mul_full_u64(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+#pragma unroll
+  for (int j = 0; j < 2 * K; ++j) t[j] = 0u;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      uint64_t p = (uint64_t)a[j] * b[i] + t[i + j] + c;
+      t[i + j] = (uint32_t)p;
+      c = (uint32_t)(p >> 32);
+    }
+    t[i + K] = c;
+  }
+}
+
+template <int K>
+WM_DEV void mul_hi_trunc_u64(uint32_t (&h)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  constexpr int C0 = (K > 2) ? K - 2 : 0;
+  constexpr int W = 2 * K - C0;
+  uint32_t acc[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) acc[j] = 0u;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const int j0 = (C0 - i) > 0 ? (C0 - i) : 0;
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (j < j0) continue;
+      uint64_t p = (uint64_t)a[j] * b[i] + acc[i + j - C0] + c;
+      acc[i + j - C0] = (uint32_t)p;
+      c = (uint32_t)(p >> 32);
+    }
+    acc[i + K - C0] = c;
+  }
+#pragma unroll
+  for (int j = 0; j < K; ++j) h[j] = acc[K - C0 + j];
+}
+
+template <int K>
+WM_DEV void mul_lo_acc_u64(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j + i < K - 1; ++j) {
+      uint64_t p = (uint64_t)a[j] * b[i] + r[i + j] + c;
+      r[i + j] = (uint32_t)p;
+      c = (uint32_t)(p >> 32);
+    }
+    r[K - 1] += a[K - 1 - i] * b[i] + c;
+  }
+}
+
+// Style selection: PTX chains (balanced IMAD.WIDE / IADD3) are faster inside
+// the NTT butterfly; compiler-chosen carries (more IMAD.X on the FMA pipe) are
+// faster for the stand-alone Barrett multiply (tools/ab_timing.py:
+// NTT 12.2 vs 12.6 us/transform, vmul 3.56 vs 3.93 TB/s).
+enum MulStyle { kPtx = 0, kU64 = 1 };
+
+template <int K, int ST = kPtx>
+WM_DEV void mul_full(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  if constexpr (ST == kPtx) mul_full_ptx<K>(t, a, b); else mul_full_u64<K>(t, a, b);
+}
+template <int K, int ST = kPtx>
+WM_DEV void mul_hi_trunc(uint32_t (&h)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  if constexpr (ST == kPtx) mul_hi_trunc_ptx<K>(h, a, b); else mul_hi_trunc_u64<K>(h, a, b);
+}
+template <int K, int ST = kPtx>
+WM_DEV void mul_lo_acc(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  if constexpr (ST == kPtx) mul_lo_acc_ptx<K>(r, a, b); else mul_lo_acc_u64<K>(r, a, b);
+}
+
 
 // ------------------------------------------------------------------ Shoup
 // Multiply by a fixed operand w with precomputed wp = floor(w * 2^(32K) / p)
@@ -369,21 +446,32 @@ WM_DEV void shr_small(uint32_t (&r)[K], const uint32_t (&a)[K], uint32_t s) {
 // q3 is within 3 of the true quotient, so r < 4 qn and two conditional
 // subtractions (2qn, then qn) make it canonical.  Cost: K^2 + ~K^2/2 + K(K+1)/2
 // word products (reference lowering: 3 K^2).
+// Default multiplier style for the Barrett path per limb count (A/B:
+// tools/ab_timing.py; WM_BARRETT_FORCE=0/1 overrides for experiments).
 template <int K>
+constexpr int barrett_style() {
+#if defined(WM_BARRETT_FORCE)
+  return WM_BARRETT_FORCE;
+#else
+  return K <= 12 ? kU64 : kPtx;
+#endif
+}
+
+template <int K, int ST = barrett_style<K>()>
 WM_DEV void mul_barrett_pre(uint32_t (&r)[K], const uint32_t (&a_shifted)[K], const uint32_t (&b)[K],
                             const FieldConst<K> &F) {
   uint32_t t[2 * K];
-  mul_full<K>(t, a_shifted, b);
+  mul_full<K, ST>(t, a_shifted, b);
   // q1 = t >> (M - 1) = t >> (32K - 5): limbs K-1 .. 2K-1 shifted by 27.
   uint32_t q1[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) q1[j] = __funnelshift_r(t[K - 1 + j], (j + K < 2 * K) ? t[K + j] : 0u, 27);
   uint32_t q3[K];
-  mul_hi_trunc<K>(q3, q1, F.mu8);
+  mul_hi_trunc<K, ST>(q3, q1, F.mu8);
   uint32_t rr[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) rr[j] = t[j];
-  mul_lo_acc<K>(rr, q3, F.nqn);
+  mul_lo_acc<K, ST>(rr, q3, F.nqn);
   cond_sub<K>(rr, F.qn2);
   cond_sub<K>(rr, F.qn);
   shr_small<K>(r, rr, F.s);

@@ -153,10 +153,14 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
         bf_lazy<K>(x0, x1, w, wp, c.p, c.p2, c.np);
         bf_lazy<K>(x2, x3, w, wp, c.p, c.p2, c.np);
       }
-      const int i2 = j << (lq - s);
-      S::load(w, tww, i2);
-      S::load(wp, twp, i2);
-      bf_lazy<K>(x0, x2, w, wp, c.p, c.p2, c.np);
+      if (s == 0) {
+        bf_lazy_w1<K>(x0, x2, c.p2);  // j = 0: root^0
+      } else {
+        const int i2 = j << (lq - s);
+        S::load(w, tww, i2);
+        S::load(wp, twp, i2);
+        bf_lazy<K>(x0, x2, w, wp, c.p, c.p2, c.np);
+      }
       const int i3 = (j + h) << (lq - s);
       S::load(w, tww, i3);
       S::load(wp, twp, i3);

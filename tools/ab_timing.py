@@ -1,0 +1,41 @@
+"""A/B timing of library variants on the headline NTT and on vmul (each
+variant in its own process: WM_LIB_PATH selects the .so)."""
+import json, os, subprocess, sys
+from pathlib import Path
+ROOT = Path(__file__).resolve().parent.parent
+CHILD = r'''
+import sys, json, statistics
+sys.path.insert(0, %r)
+import torch
+from paper_2501_07535_b200 import kernels as K, device as dev
+from paper_2501_07535_b200.params import find_ntt_params
+N, B = 1 << 16, 64
+plan = K.get_plan(256, find_ntt_params(256, N))
+x = torch.randint(0, 1 << 27, (B * N, 8), dtype=torch.int32, device="cuda")
+y = torch.empty_like(x); z = torch.empty_like(x)
+ws = torch.empty(plan.workspace_bytes(B) // 4, dtype=torch.int32, device="cuda")
+def t(fn, reps=10):
+    for _ in range(3): fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+    for a, b in ev:
+        a.record(); fn(); b.record()
+    torch.cuda.synchronize()
+    return statistics.median(a.elapsed_time(b) for a, b in ev)
+ms = t(lambda: (plan.forward(x, out=y, workspace=ws), plan.inverse(y, out=z, workspace=ws)))
+assert torch.equal(z, x)
+res = {"ntt_step_ms": ms, "us_per_transform": ms * 1e3 / 128}
+for bits in (128, 256, 384, 768):
+    Kl = bits // 32
+    f = dev.Field(bits, find_ntt_params(bits, 1).p)
+    n = 1 << 22
+    a = torch.randint(0, 1 << 27, (n, Kl), dtype=torch.int32, device="cuda"); b = a.flip(0).contiguous()
+    o = torch.empty_like(a)
+    mv = t(lambda: f.vmul(a, b, out=o))
+    res[f"vmul{bits}_GBps"] = round(3 * 4 * Kl * n / mv / 1e6, 1)
+print(json.dumps(res))
+''' % str(ROOT)
+for lib in sys.argv[1:]:
+    env = dict(os.environ, WM_LIB_PATH=str(ROOT / lib))
+    out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
+    print(lib, out.stdout.strip() or out.stderr[-2000:])
