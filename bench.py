@@ -207,11 +207,12 @@ def run_gpu(args, rank, world, local, pg):
             step()
             ev[s][1].record(stream)
         torch.cuda.synchronize()
-        # forward transform alone (its launches), for the roofline of the NTT passes
+        # the dominant kernel alone (pass 0 = ntt_col_pass, 45% of the step in the
+        # ncu launch list profiles/r01_launches_bench.csv), for the roofline
         for s in range(args.steps):
             flush_l2(torch, flush)
             fwd_ev[s][0].record(stream)
-            plan.forward(x, out=y, workspace=ws)
+            plan.run_pass(0, x, y)
             fwd_ev[s][1].record(stream)
         torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -221,7 +222,7 @@ def run_gpu(args, rank, world, local, pg):
     transforms = world * args.steps * 2 * BATCH
     us_per_transform = total_ms * 1e3 / transforms
 
-    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
+    pass0_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
 
     # ---- end-to-end through the C ABI with host buffers (reference layout)
     e2e = run_e2e(args, torch, dev, plan, field, ws, pg, world)
@@ -234,7 +235,7 @@ def run_gpu(args, rank, world, local, pg):
     return {
         "us_per_transform": us_per_transform,
         "ms_per_step": total_ms / args.steps,
-        "fwd_ms": fwd_ms,
+        "pass0_ms": pass0_ms,
         "pass_log_sizes": plan.pass_log_sizes,
         "launches_per_step": launches_per_step,
         "clocks": clocks.summary(),
@@ -571,22 +572,29 @@ def main():
             pg.destroy_process_group()
         return
 
-    # roofline of the dominant kernel: the NTT passes (integer pipe)
+    # roofline of the dominant kernel: ntt_col_pass (pass 0), integer pipe
     sizes = res["pass_log_sizes"]
     peak, clk = int_peak_wmul_per_s(res["clocks"].get("sm_mhz"))
-    # full-transform average per launch (passes are near-identical in work)
-    fwd_ms = res["fwd_ms"]  # one forward batch (its pass launches), L2 flushed before
-    bflies_fwd = BATCH * (N // 2) * LOGN
-    achieved = bflies_fwd * ALG_WMUL_PER_BFLY / (fwd_ms * 1e-3)
+    pass_ms = res["pass0_ms"]
+    bflies = BATCH * (N // 2) * sizes[0]  # one pass = log2(L) radix-2 stages over the batch
+    achieved = bflies * ALG_WMUL_PER_BFLY / (pass_ms * 1e-3)
+    traffic = None
+    try:
+        prof = json.loads((ROOT / "profiles" / "r01_ncu_traffic.json").read_text())
+        traffic = prof["ntt_col_pass<8>"]["dram_bytes_per_launch"]
+    except Exception:
+        pass
     roofline = {
         "bound": "int", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Twmul/s",
-        "frac": achieved / peak, "traffic": None,
-        "kernel": f"ntt_col_pass/ntt_row_pass ({'+'.join('2^%d' % s for s in sizes)} passes), forward batch 64",
-        "work": f"{ALG_WMUL_PER_BFLY} word products per butterfly (reference 3k^2, SURVEY.md §8(d)) x "
-                f"(n/2) log2 n butterflies",
+        "frac": achieved / peak, "traffic": traffic,
+        "kernel": f"ntt_col_pass<8> (pass 0 of {'+'.join('2^%d' % s for s in sizes)}), batch 64, {pass_ms * 1e3:.1f} us/launch",
+        "work": f"{ALG_WMUL_PER_BFLY} word products per butterfly (reference 3k^2, SURVEY.md \u00a78(d)) x "
+                f"batch*(n/2)*log2(L) butterflies per launch = {bflies * ALG_WMUL_PER_BFLY:.4g}",
         "peak_basis": f"32 IMAD.WIDE/clk/SM x 148 SMs x {clk:.0f} MHz (half-rate IMAD.WIDE measured, "
                       f"profiles/r01_imad_rate.jsonl)",
-        "ns_per_butterfly_paper_metric": 2 * (fwd_ms * 1e6 / BATCH) / (N * LOGN),
+        "traffic_basis": "dram__bytes_read+write per launch, ncu --set full (profiles/r01_ncu_traffic.json); "
+                         "algorithmic bytes per launch = 2 x 128 MiB",
+        "ns_per_butterfly_paper_metric": 2 * (res["ms_per_step"] * 1e6 / (2 * BATCH)) / (N * LOGN),
     }
     cpu = None
     if world == 1:

@@ -124,6 +124,21 @@ int wm_ntt_forward(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int6
 int wm_ntt_inverse(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int64_t batch,
                    void *workspace, void *stream);
 
+/* Cyclic convolution of each pair of length-n vectors (batch of them):
+ * out = INTT(NTT(a) * NTT(b)) — the reference's own convolution check
+ * (verify.py:195-223: run_ntt, run_vector(vmul), run_ntt(intt)) as three
+ * launch sequences, with the pointwise product fused into the epilogue of
+ * the forward transform of b.  a may alias out; b may not. */
+int wm_ntt_convolve(const wm_ntt_plan *p, const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t batch,
+                    void *workspace, void *stream);
+
+/* Diagnostic: launch pass `pass_index` of the forward/inverse transform
+ * alone, from `in` to `out` (distinct buffers), e.g. to time one kernel with
+ * events.  Intermediate passes leave values in [0, 4p); only the full
+ * wm_ntt_forward/inverse sequence is the transform. */
+int wm_ntt_pass(const wm_ntt_plan *p, int inverse, int pass_index, const uint32_t *in, uint32_t *out,
+                int64_t batch, void *stream);
+
 /* Copies twiddle powers root^e (inverse: root_inv^e) for e in [0, count) into
  * out (device, count*K limbs): the reference twiddle_table (kernels.py:259-267)
  * is the first n/2 of them. */

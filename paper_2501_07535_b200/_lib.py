@@ -60,6 +60,8 @@ SIGNATURES = [
     ("wm_ntt_workspace_bytes", _i64, [_vp, _i64]),
     ("wm_ntt_forward", _int, [_vp, _vp, _vp, _i64, _vp, _vp]),
     ("wm_ntt_inverse", _int, [_vp, _vp, _vp, _i64, _vp, _vp]),
+    ("wm_ntt_convolve", _int, [_vp, _vp, _vp, _vp, _i64, _vp, _vp]),
+    ("wm_ntt_pass", _int, [_vp, _int, _int, _vp, _vp, _i64, _vp]),
     ("wm_ntt_twiddles", _int, [_vp, _int, _i64, _vp, _vp]),
     ("wm_ntt_host", _int, [_vp, _int, _int, _int, _vp, _vp, _i64, _i64, _vp]),
     ("wm_transpose", _int, [_int, _vp, _vp, _i64, _i64, _i64, _vp]),

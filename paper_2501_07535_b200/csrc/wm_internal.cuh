@@ -61,7 +61,7 @@ struct wm_field {
   wm::Big q, qn, qn2, nqn, mu8;  // K limbs each
 };
 
-struct wm_ntt_pass {
+struct wm_pass_plan {
   bool column = false;  // column pass (strided lines) vs row pass (contiguous lines)
   int logL = 0;         // sub-transform size
   int G = 1;            // lines per CTA
@@ -83,7 +83,7 @@ struct wm_ntt_plan {
   int K = 0;
   int64_t n = 0;
   int logn = 0;
-  std::vector<wm_ntt_pass> passes;
+  std::vector<wm_pass_plan> passes;
   // device tables: n entries of (w, w') pairs (2K words each)
   uint32_t *tw_fwd = nullptr, *tw_inv = nullptr, *tw_inv_scaled = nullptr;
   wm::Big ninv, ninv_sh, np, p2;  // n^-1, floor(n^-1 * 2^32K / p), 2^32K - p, 2p
@@ -103,6 +103,6 @@ struct wm_ntt_plan {
 
 namespace wm {
 int ntt_run_internal(const wm_ntt_plan *p, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
-                     void *workspace, cudaStream_t st);
+                     void *workspace, cudaStream_t st, const uint32_t *mul_by = nullptr);
 int release_host_pipeline(wm_ntt_plan *p);
 }  // namespace wm

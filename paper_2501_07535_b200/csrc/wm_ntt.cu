@@ -36,6 +36,7 @@ namespace wm {
 
 template <int K>
 struct NttConst {
+  FieldConst<K> F;  // Barrett constants of p (pointwise-product epilogue)
   uint32_t p[K];
   uint32_t p2[K];   // 2p
   uint32_t np[K];   // 2^(32K) - p
@@ -55,6 +56,7 @@ struct PassDesc {
   int canonical_out;  // last pass: reduce [0, 4p) -> [0, p)
   int64_t tw_stride;  // n / L
   int64_t total_lines;  // row passes: batch * lines_inner
+  const uint32_t *mul_by;  // last pass: out[pos] = result[pos] * mul_by[pos] mod p (convolution)
 };
 
 // ------------------------------------------------------------------ smem layout
@@ -235,6 +237,12 @@ __global__ void __launch_bounds__(256) ntt_col_pass(const uint32_t *in, uint32_t
     }
     if (d.canonical_out) canonical_4p<K>(v, c.p, c.p2);
     const int64_t pos = base + o * d.WO + (int64_t)k * d.WK + i0 + g;
+    if (d.mul_by) {
+      uint32_t m[K], rr[K];
+      ldg_elem<K>(m, d.mul_by + pos * K);
+      mul_barrett<K>(rr, v, m, c.F);
+      copy_n<K>(v, rr);
+    }
     stg_elem<K>(out + pos * K, v);
   }
 }
@@ -282,6 +290,12 @@ __global__ void __launch_bounds__(256) ntt_row_pass(const uint32_t *in, uint32_t
       }
       if (d.canonical_out) canonical_4p<K>(v, c.p, c.p2);
       const int64_t pos = b * d.n + r * d.WO + (int64_t)k * d.WK;
+      if (d.mul_by) {  // fused pointwise product (NTT-domain convolution)
+        uint32_t m[K], rr[K];
+        ldg_elem<K>(m, d.mul_by + pos * K);
+        mul_barrett<K>(rr, v, m, c.F);
+        copy_n<K>(v, rr);
+      }
       stg_elem<K>(out + pos * K, v);
     }
   }
@@ -369,6 +383,7 @@ static int gen_table(const wm_field *f, uint32_t *table, int64_t count, const Bi
 template <int K>
 static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
   NttConst<K> c;
+  c.F = field_const_local<K>(pl->field);
   for (int j = 0; j < K; ++j) {
     c.p[j] = pl->field->q[j];
     c.p2[j] = pl->p2[j];
@@ -379,14 +394,15 @@ static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
   return c;
 }
 
-static size_t pass_smem(int K, const wm_ntt_pass &ps) {
+static size_t pass_smem(int K, const wm_pass_plan &ps) {
   const size_t L = (size_t)1 << ps.logL;
   return ((size_t)ps.G * L * K + (L / 2) * 2 * (size_t)K) * sizeof(uint32_t);
 }
 
 template <int K>
 static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
-                      uint32_t *ws, cudaStream_t st) {
+                      uint32_t *ws, cudaStream_t st, int only_pass = -1,
+                      const uint32_t *mul_by = nullptr) {
   static bool attr_done = false;
   if (!attr_done) {
     WM_CUDA_TRY(cudaFuncSetAttribute(ntt_col_pass<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
@@ -395,9 +411,15 @@ static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, u
   }
   const NttConst<K> c = ntt_const<K>(pl);
   const uint32_t *tw_sub = inverse ? pl->tw_inv : pl->tw_fwd;
-  for (const wm_ntt_pass &ps : pl->passes) {
+  for (int pi = 0; pi < (int)pl->passes.size(); ++pi) {
+    if (only_pass >= 0 && pi != only_pass) continue;
+    const wm_pass_plan &ps = pl->passes[pi];
     const uint32_t *src = ps.src == 0 ? in : (ps.src == 1 ? ws : out);
     uint32_t *dst = ps.dst == 0 ? out : ws;
+    if (only_pass >= 0) {  // diagnostic single-pass launch: caller's buffers
+      src = in;
+      dst = out;
+    }
     PassDesc d;
     d.n = pl->n;
     d.logL = ps.logL;
@@ -416,6 +438,7 @@ static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, u
     d.canonical_out = ps.canonical_out ? 1 : 0;
     d.tw_stride = pl->n >> ps.logL;
     d.total_lines = batch * ps.lines_inner;
+    d.mul_by = (pi + 1 == (int)pl->passes.size()) ? mul_by : nullptr;
     const size_t smem = pass_smem(K, ps);
     if (ps.column) {
       const uint32_t *tw_out = inverse ? (ps.scaled_table ? pl->tw_inv_scaled : pl->tw_inv) : pl->tw_fwd;
@@ -453,7 +476,7 @@ static int plan_passes(wm_ntt_plan *pl) {
   pl->passes.clear();
   const int64_t n = pl->n;
   if (P == 1) {
-    wm_ntt_pass a;
+    wm_pass_plan a;
     a.column = false;
     a.logL = logn;
     a.G = choose_G(logn, 1 << 20);
@@ -467,7 +490,7 @@ static int plan_passes(wm_ntt_plan *pl) {
   } else if (P == 2) {
     const int logN2 = sizes[0], logN1 = sizes[1];
     const int64_t N1 = (int64_t)1 << logN1, N2 = (int64_t)1 << logN2;
-    wm_ntt_pass a;  // N2-point DFTs over j2 (stride N1), twiddle root^(j1*k2)
+    wm_pass_plan a;  // N2-point DFTs over j2 (stride N1), twiddle root^(j1*k2)
     a.column = true;
     a.logL = logN2;
     a.G = choose_G(logN2, N1);
@@ -484,7 +507,7 @@ static int plan_passes(wm_ntt_plan *pl) {
     a.scaled_table = true;
     a.src = 0;
     a.dst = 1;
-    wm_ntt_pass b;  // N1-point DFTs over contiguous j1, transposing store
+    wm_pass_plan b;  // N1-point DFTs over contiguous j1, transposing store
     b.column = false;
     b.logL = logN1;
     b.G = choose_G(logN1, 1 << 20);
@@ -499,7 +522,7 @@ static int plan_passes(wm_ntt_plan *pl) {
     const int logM2 = sizes[0], logM1 = sizes[1], logN1 = sizes[2];
     const int64_t N1 = (int64_t)1 << logN1, M1 = (int64_t)1 << logM1, M2 = (int64_t)1 << logM2;
     const int64_t N2 = M1 * M2;
-    wm_ntt_pass a;  // M2-point DFTs over b, lines i = j1 + N1*a; twiddle root^(N1*a*c)
+    wm_pass_plan a;  // M2-point DFTs over b, lines i = j1 + N1*a; twiddle root^(N1*a*c)
     a.column = true;
     a.logL = logM2;
     a.G = choose_G(logM2, N1 * M1);
@@ -514,7 +537,7 @@ static int plan_passes(wm_ntt_plan *pl) {
     a.scaled_table = false;
     a.src = 0;
     a.dst = 0;
-    wm_ntt_pass b;  // M1-point DFTs over a, lines (o=c, i=j1); twiddle root^(j1*(c + M2*d))
+    wm_pass_plan b;  // M1-point DFTs over a, lines (o=c, i=j1); twiddle root^(j1*(c + M2*d))
     b.column = true;
     b.logL = logM1;
     b.G = choose_G(logM1, N1);
@@ -531,7 +554,7 @@ static int plan_passes(wm_ntt_plan *pl) {
     b.scaled_table = true;
     b.src = 2;  // reads `out` (written by pass a)
     b.dst = 1;
-    wm_ntt_pass cc;  // N1-point DFTs over contiguous j1, transposing store
+    wm_pass_plan cc;  // N1-point DFTs over contiguous j1, transposing store
     cc.column = false;
     cc.logL = logN1;
     cc.G = choose_G(logN1, 1 << 20);
@@ -669,7 +692,7 @@ int64_t wm_ntt_workspace_bytes(const wm_ntt_plan *p, int64_t batch) {
 
 namespace wm {
 int ntt_run_internal(const wm_ntt_plan *pc, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
-                     void *workspace, cudaStream_t stream) {
+                     void *workspace, cudaStream_t stream, const uint32_t *mul_by) {
   if (!pc) return fail(WM_EINVAL, "null plan");
   if (batch < 0) return fail(WM_EINVAL, "negative batch");
   if (batch == 0) return WM_OK;
@@ -697,7 +720,7 @@ int ntt_run_internal(const wm_ntt_plan *pc, bool inverse, const uint32_t *in, ui
   switch (p->K) {
 #define WM_CASE(k) \
   case k:          \
-    return run_passes<k>(p, inverse, in, out, batch, ws, st);
+    return run_passes<k>(p, inverse, in, out, batch, ws, st, -1, mul_by);
     WM_NTT_KS(WM_CASE)
 #undef WM_CASE
     default:
@@ -721,6 +744,36 @@ int wm_ntt_forward(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int6
 int wm_ntt_inverse(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int64_t batch, void *workspace,
                    void *stream) {
   return ntt_run(p, true, in, out, batch, workspace, stream);
+}
+
+int wm_ntt_convolve(const wm_ntt_plan *p, const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t batch,
+                    void *workspace, void *stream) {
+  if (!p) return fail(WM_EINVAL, "null plan");
+  if (!a || !b || !out) return fail(WM_EINVAL, "null data pointer");
+  if (b == out && a != out) return fail(WM_EINVAL, "b may not alias out (out holds NTT(a) while b is read)");
+  if (b == out) return fail(WM_EINVAL, "a and b may not both alias out");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ntt_run_internal(p, false, a, out, batch, workspace, st, nullptr);  // out = NTT(a)
+  if (rc) return rc;
+  rc = ntt_run_internal(p, false, b, out, batch, workspace, st, out);  // out = NTT(b) * NTT(a), fused
+  if (rc) return rc;
+  return ntt_run_internal(p, true, out, out, batch, workspace, st, nullptr);  // out = INTT(...)
+}
+
+int wm_ntt_pass(const wm_ntt_plan *p, int inverse, int pass_index, const uint32_t *in, uint32_t *out,
+                int64_t batch, void *stream) {
+  if (!p) return fail(WM_EINVAL, "null plan");
+  if (pass_index < 0 || pass_index >= (int)p->passes.size()) return fail(WM_EINVAL, "pass index out of range");
+  if (batch <= 0 || !in || !out || in == out) return fail(WM_EINVAL, "bad buffers/batch");
+  switch (p->K) {
+#define WM_CASE(k) \
+  case k:          \
+    return run_passes<k>(p, inverse != 0, in, out, batch, nullptr, (cudaStream_t)stream, pass_index);
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      return fail(WM_EUNSUPPORTED, "limb count not built into the NTT kernels");
+  }
 }
 
 int wm_ntt_twiddles(const wm_ntt_plan *p, int inverse, int64_t count, uint32_t *out, void *stream) {

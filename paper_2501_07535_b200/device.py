@@ -255,6 +255,33 @@ class NttPlan:
         """x[j] = n^-1 sum_k y[k] root^(-jk) mod p per transform."""
         return self._run(self.lib.wm_ntt_inverse, x, out, workspace, stream)
 
+    def convolve(self, a, b, out=None, workspace=None, stream=None):
+        """Cyclic convolution per transform: INTT(NTT(a) * NTT(b)) with the
+        pointwise product fused into the forward transform of b."""
+        torch = _torch()
+        if a.numel() != b.numel():
+            raise ValueError("a and b differ in size")
+        if out is None:
+            out = torch.empty_like(a)
+        if out.data_ptr() == b.data_ptr():
+            raise ValueError("b may not alias out")
+        K = self.limbs
+        total = a.numel() // K
+        if total % self.n:
+            raise ValueError(f"expected a multiple of {self.n} elements")
+        batch = total // self.n
+        ws = _ptr(workspace) if workspace is not None else None
+        _lib.check(self.lib.wm_ntt_convolve(self._h, _ptr(a), _ptr(b), _ptr(out), batch, ws, _stream_ptr(stream)),
+                   "wm_ntt_convolve")
+        return out
+
+    def run_pass(self, pass_index: int, x, out, inverse: bool = False, stream=None):
+        """Diagnostic: one pass kernel alone (wm_ntt_pass), for timing."""
+        batch = x.numel() // (self.limbs * self.n)
+        _lib.check(self.lib.wm_ntt_pass(self._h, 1 if inverse else 0, pass_index, _ptr(x), _ptr(out), batch,
+                                        _stream_ptr(stream)), "wm_ntt_pass")
+        return out
+
     def host_transform(self, host_in, host_out, mode: str = "forward", word_bits: int = 64,
                        ref_words: int | None = None, chunk: int = 0, stream=None):
         """End-to-end transform of HOST tensors in the reference layout (AoS,

@@ -6,7 +6,7 @@ import subprocess
 import sys
 
 KEYS = [
-    ("gpu__time_duration.sum", "duration_ns"),
+    ("gpu__time_duration.sum", "duration_us"),
     ("sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed", "fmaheavy_pct"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_elapsed", "fma_pct"),
     ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_elapsed", "alu_pct"),
@@ -36,6 +36,9 @@ def summarise(rep):
     txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     hdr = rows[0]
+    units = dict(zip(hdr, rows[1]))
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+             "nsecond": 1, "usecond": 1e3, "msecond": 1e6}
     out = []
     for row in rows[2:]:
         d = dict(zip(hdr, row))
@@ -43,7 +46,9 @@ def summarise(rep):
         for k, name in KEYS:
             if k in d:
                 try:
-                    rec[name] = float(d[k].replace(",", ""))
+                    v = float(d[k].replace(",", ""))
+                    v *= scale.get(units.get(k, ""), 1)  # bytes -> bytes, time -> ns
+                    rec[name] = v
                 except ValueError:
                     rec[name] = d[k]
         out.append(rec)
