@@ -484,7 +484,8 @@ def run_cpu_reference(transforms: int):
     cores; falls back to the C oracle port when _ref was not built."""
     cores = len(os.sched_getaffinity(0))
     lib = _ref_lib()
-    half = max(1, transforms // 2)
+    # at least one transform per core in each direction so every core works
+    half = max(1, transforms // 2, cores)
     if lib is not None:
         x = cpu_sample_inputs(half)
         y = x.copy()

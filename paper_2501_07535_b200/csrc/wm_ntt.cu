@@ -32,6 +32,16 @@
 #include "wm_internal.cuh"
 #include "wm_io.cuh"
 
+// Minimum resident CTAs per SM requested from ptxas for the pass kernels
+// (caps registers at 65536 / (256 * WM_NTT_MINB)); A/B: tools/ab_timing.py.
+#ifndef WM_NTT_MINB
+#define WM_NTT_MINB 2
+#endif
+// Target tile size (32-bit words of data per CTA; 16384 = 64 KB).
+#ifndef WM_NTT_TILE_WORDS
+#define WM_NTT_TILE_WORDS 16384
+#endif
+
 namespace wm {
 
 template <int K>
@@ -117,6 +127,33 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
                                          int G, const NttConst<K> &c) {
   using S = Smem<K>;
   const int L = 1 << logL;
+#if defined(WM_NTT_RADIX2)
+  for (int s = 0; s < logL; ++s) {
+    const int h = 1 << s;
+    for (int bf = threadIdx.x; bf < (G * L) >> 1; bf += blockDim.x) {
+      const int g = bf >> (logL - 1);
+      const int jj = bf & ((L >> 1) - 1);
+      const int j = jj & (h - 1);
+      const int e0 = (g << logL) + ((jj >> s) << (s + 1)) + j;
+      uint32_t x0[K], x1[K];
+      S::load(x0, data, e0);
+      S::load(x1, data, e0 + h);
+      if (s == 0) {
+        bf_lazy_w1<K>(x0, x1, c.p2);
+      } else {
+        uint32_t w[K], wp[K];
+        const int i1 = j << (logL - 1 - s);
+        S::load(w, tww, i1);
+        S::load(wp, twp, i1);
+        bf_lazy<K>(x0, x1, w, wp, c.p, c.p2, c.np);
+      }
+      S::store(data, e0, x0);
+      S::store(data, e0 + h, x1);
+    }
+    __syncthreads();
+  }
+  return;
+#endif
   int s = 0;
   if (logL & 1) {  // stage 0 alone: pairs (2m, 2m+1), twiddle 1
     for (int bf = threadIdx.x; bf < (G * L) >> 1; bf += blockDim.x) {
@@ -196,7 +233,7 @@ __device__ __forceinline__ size_t tile_words(int logL, int G) {
 // ------------------------------------------------------------------ column pass
 // Line (o, i), i in [0, lines_inner) consecutive per CTA (G of them).
 template <int K>
-__global__ void __launch_bounds__(256) ntt_col_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
+__global__ void __launch_bounds__(256, WM_NTT_MINB) ntt_col_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
                                                     const uint32_t *tw_out, const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -250,7 +287,7 @@ __global__ void __launch_bounds__(256) ntt_col_pass(const uint32_t *in, uint32_t
 // ------------------------------------------------------------------ row pass
 // Line lambda in [0, batch * lines_inner): b = lambda / R, r = lambda % R.
 template <int K>
-__global__ void __launch_bounds__(256) ntt_row_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
+__global__ void __launch_bounds__(256, WM_NTT_MINB) ntt_row_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
                                                     const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -467,7 +504,7 @@ static int plan_passes(wm_ntt_plan *pl) {
   for (int i = 0; i < logn % P; ++i) sizes[i] += 1;
   auto choose_G = [&](int logL, int64_t inner_cap) {
     int64_t words_line = ((int64_t)1 << logL) * K;
-    int64_t G = std::max<int64_t>(1, 16384 / words_line);  // ~64 KB of data per CTA
+    int64_t G = std::max<int64_t>(1, WM_NTT_TILE_WORDS / words_line);  // data words per CTA
     G = std::min<int64_t>(G, 32);
     int64_t g = 1;
     while (g * 2 <= G) g *= 2;
