@@ -463,6 +463,9 @@ def run_reference_gpu(args, torch, plan):
 # ------------------------------------------------------------ CPU baselines
 def _ref_lib():
     os.environ.setdefault("OMP_STACKSIZE", "64M")
+    # all host cores (torchrun exports OMP_NUM_THREADS=1 to every rank; the
+    # reference arm runs on rank 0 alone and should use the whole host)
+    os.environ["OMP_NUM_THREADS"] = str(len(os.sched_getaffinity(0)))
     path = ROOT / "oracle" / "_ref" / "libref_cpu.so"
     if not path.exists():
         return None

@@ -117,6 +117,35 @@ struct Smem {
 };
 
 // ------------------------------------------------------------------ in-smem DFT
+// One radix-4 group (stages s, s+1) with one product at a time (wide K,
+// where two interleaved products would spill registers).
+template <int K>
+__device__ __forceinline__ void radix4_single(uint32_t (&x0)[K], uint32_t (&x1)[K], uint32_t (&x2)[K],
+                                              uint32_t (&x3)[K], const uint32_t *tww, const uint32_t *twp, int s,
+                                              int j, int h, int logL, int lq, const NttConst<K> &c) {
+  using S = Smem<K>;
+  uint32_t w[K], wp[K];
+  if (s == 0) {
+    bf_lazy_w1<K>(x0, x1, c.p2);
+    bf_lazy_w1<K>(x2, x3, c.p2);
+    bf_lazy_w1<K>(x0, x2, c.p2);  // j = 0: root^0
+  } else {
+    const int i1 = j << (logL - 1 - s);
+    S::load(w, tww, i1);
+    S::load(wp, twp, i1);
+    bf_lazy<K>(x0, x1, w, wp, c.p, c.p2, c.np);
+    bf_lazy<K>(x2, x3, w, wp, c.p, c.p2, c.np);
+    const int i2 = j << (lq - s);
+    S::load(w, tww, i2);
+    S::load(wp, twp, i2);
+    bf_lazy<K>(x0, x2, w, wp, c.p, c.p2, c.np);
+  }
+  const int i3 = (j + h) << (lq - s);
+  S::load(w, tww, i3);
+  S::load(wp, twp, i3);
+  bf_lazy<K>(x1, x3, w, wp, c.p, c.p2, c.np);
+}
+
 // G lines of L = 2^logL elements (tile element g*L + pos), bit-reversed order
 // on entry, natural order on exit, values in [0, 4p) throughout.  Stages run
 // two at a time as radix-4 groups held in registers (one shared-memory round
@@ -182,28 +211,8 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
       S::load(x2, data, e0 + 2 * h);
       S::load(x3, data, e0 + 3 * h);
       uint32_t w[K], wp[K];
-      if (s == 0) {
-        bf_lazy_w1<K>(x0, x1, c.p2);
-        bf_lazy_w1<K>(x2, x3, c.p2);
-      } else {
-        const int i1 = j << (logL - 1 - s);
-        S::load(w, tww, i1);
-        S::load(wp, twp, i1);
-        bf_lazy<K>(x0, x1, w, wp, c.p, c.p2, c.np);
-        bf_lazy<K>(x2, x3, w, wp, c.p, c.p2, c.np);
-      }
-      if (s == 0) {
-        bf_lazy_w1<K>(x0, x2, c.p2);  // j = 0: root^0
-      } else {
-        const int i2 = j << (lq - s);
-        S::load(w, tww, i2);
-        S::load(wp, twp, i2);
-        bf_lazy<K>(x0, x2, w, wp, c.p, c.p2, c.np);
-      }
-      const int i3 = (j + h) << (lq - s);
-      S::load(w, tww, i3);
-      S::load(wp, twp, i3);
-      bf_lazy<K>(x1, x3, w, wp, c.p, c.p2, c.np);
+      radix4_single<K>(x0, x1, x2, x3, tww, twp, s, j, h, logL, lq, c);
+
       S::store(data, e0, x0);
       S::store(data, e0 + h, x1);
       S::store(data, e0 + 2 * h, x2);
@@ -233,7 +242,7 @@ __device__ __forceinline__ size_t tile_words(int logL, int G) {
 // ------------------------------------------------------------------ column pass
 // Line (o, i), i in [0, lines_inner) consecutive per CTA (G of them).
 template <int K>
-__global__ void __launch_bounds__(256, WM_NTT_MINB) ntt_col_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
+__global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
                                                     const uint32_t *tw_out, const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -287,7 +296,7 @@ __global__ void __launch_bounds__(256, WM_NTT_MINB) ntt_col_pass(const uint32_t 
 // ------------------------------------------------------------------ row pass
 // Line lambda in [0, batch * lines_inner): b = lambda / R, r = lambda % R.
 template <int K>
-__global__ void __launch_bounds__(256, WM_NTT_MINB) ntt_row_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
+__global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
                                                     const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
