@@ -470,6 +470,10 @@ def _ref_lib():
     if not path.exists():
         return None
     lib = ctypes.CDLL(str(path))
+    try:  # libgomp may have been initialised before we set the variable
+        ctypes.CDLL("libgomp.so.1").omp_set_num_threads(len(os.sched_getaffinity(0)))
+    except OSError:
+        pass
     for nm in ("refdrv_ntt65536_256w64", "refdrv_intt65536_256w64"):
         getattr(lib, nm).argtypes = [ctypes.c_void_p, ctypes.c_int64]
     return lib
