@@ -88,8 +88,8 @@ def test_emitted_launchers_run(cuda, tmp_path):
     ys = torch.randint(0, 1 << 27, (100, 4), dtype=torch.int32, device="cuda")
     s = 123456789123456789
     sref = fa.to_ref_layout(dev.to_device(dev.ints_to_limbs([s], 4)), 32, 4)
-    out = torch.empty_like(fa.to_ref_layout(xs, 32, 4))
-    f3(sref.data_ptr(), fa.to_ref_layout(xs, 32, 4).data_ptr(), fa.to_ref_layout(ys, 32, 4).data_ptr(),
-       out.data_ptr(), 100)
+    rx, ry = fa.to_ref_layout(xs, 32, 4), fa.to_ref_layout(ys, 32, 4)  # keep alive across the call
+    out = torch.empty_like(rx)
+    f3(sref.data_ptr(), rx.data_ptr(), ry.data_ptr(), out.data_ptr(), 100)
     torch.cuda.synchronize()
     assert torch.equal(fa.from_ref_layout(out, 32, 4), fa.axpy(s, xs, ys))
