@@ -230,6 +230,7 @@ def run_gpu(args, rank, world, local, pg):
     # ---- extras: BLAS sweep (configs[2]), four-step single 2^24 NTT (configs[4]), reference GPU code
     blas = run_blas(args, torch, field, pg) if not args.skip_extras else None
     four = run_four_step(args, torch, rank, world, pg) if not args.skip_extras else None
+    b20 = run_batched_2p20(args, torch, rank, world, pg) if not args.skip_extras else None
     refgpu = run_reference_gpu(args, torch, plan) if (world == 1 and not args.skip_extras) else None
 
     return {
@@ -242,6 +243,7 @@ def run_gpu(args, rank, world, local, pg):
         "e2e": e2e,
         "blas": blas,
         "four_step": four,
+        "batched_2p20": b20,
         "reference_gpu": refgpu,
     }
 
@@ -357,6 +359,41 @@ def run_four_step(args, torch, rank, world, pg):
     return {"n": n, "ranks": world, "ms_per_forward": round(ms, 4), "us_per_transform": round(ms * 1e3, 2),
             "split": [L.n1, L.n2], "a2a_bytes_sent_per_rank": a2a_bytes,
             "note": "max over ranks; forward only; input rows j1 per rank (scatter not timed)"}
+
+
+def run_batched_2p20(args, torch, rank, world, pg):
+    """BASELINE configs[3]: 256-bit NTT n=2^20, batch 256 in total, sharded by
+    batch across the ranks (strong scaling, no collective): forward + inverse."""
+    from paper_2501_07535_b200 import dist as D
+    from paper_2501_07535_b200 import kernels as K
+    from paper_2501_07535_b200.params import find_ntt_params
+    n, total = 1 << 20, 256
+    lo, hi = D.shard_range(total, rank, world)
+    b = hi - lo
+    plan = K.get_plan(BITS, find_ntt_params(BITS, n))
+    x = canonical_random(torch, b * n, 777 + rank)
+    y = torch.empty_like(x)
+    z = torch.empty_like(x)
+    ws = torch.empty(plan.workspace_bytes(b) // 4, dtype=torch.int32, device="cuda")
+    plan.forward(x, out=y, workspace=ws)
+    plan.inverse(y, out=z, workspace=ws)
+    torch.cuda.synchronize()
+    assert torch.equal(z, x), "2^20 roundtrip mismatch"
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(pg)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    plan.forward(x, out=y, workspace=ws)
+    plan.inverse(y, out=z, workspace=ws)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(pg, e0.elapsed_time(e1))
+    del x, y, z, ws
+    torch.cuda.empty_cache()
+    return {"n": n, "batch_total": total, "ranks": world, "ms_fwd_plus_inv": round(ms, 3),
+            "us_per_transform": round(ms * 1e3 / (2 * total), 2), "passes": plan.pass_log_sizes,
+            "scaling": "strong (fixed total batch 256)", "note": "max over ranks; inputs 8 GiB / world per rank"}
 
 
 class _SelfComm:
@@ -634,6 +671,7 @@ def main():
         "clocks": res["clocks"],
         "blas": res["blas"],
         "four_step_2p24": res["four_step"],
+        "batched_2p20_x256": res["batched_2p20"],
         "reference_gpu": res["reference_gpu"],
     }
     print(json.dumps(out))
