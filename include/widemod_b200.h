@@ -74,6 +74,12 @@ int wm_supported_limbs(int ntt, int *out, int cap);
  * or more generally 1 < q < 2^(32K-4) with bit length > 32K-36.
  * q is given as q_limbs little-endian 32-bit limbs (host memory). */
 int wm_field_create(int bits, const uint32_t *q_host, int q_limbs, wm_field **out);
+/* flags: WM_FIELD_KARATSUBA selects one-level (recursive for >= 16 limbs)
+ * Karatsuba full products in vmul/axpy — the reference's
+ * make_spec(..., strategy="karatsuba") (kernels.py:104-117, rewrite.py:234-253).
+ * The NTT's Shoup multiply is a truncated product and is unaffected. */
+#define WM_FIELD_KARATSUBA 1
+int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags, wm_field **out);
 int wm_field_destroy(wm_field *f);
 int wm_field_info(const wm_field *f, int *bits, int *limbs, int *norm_shift);
 

@@ -48,6 +48,7 @@ SIGNATURES = [
     ("wm_limbs_for_bits", _int, [_int]),
     ("wm_supported_limbs", _int, [_int, ctypes.POINTER(_int), _int]),
     ("wm_field_create", _int, [_int, _u32p, _int, ctypes.POINTER(_vp)]),
+    ("wm_field_create_ex", _int, [_int, _u32p, _int, _int, ctypes.POINTER(_vp)]),
     ("wm_field_destroy", _int, [_vp]),
     ("wm_field_info", _int, [_vp, ctypes.POINTER(_int), ctypes.POINTER(_int), ctypes.POINTER(_int)]),
     ("wm_vadd", _int, [_vp, _vp, _vp, _vp, _i64, _vp]),

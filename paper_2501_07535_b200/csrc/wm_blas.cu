@@ -145,7 +145,7 @@ struct BlasArgs {
   uint32_t scal[K];  // axpy scalar, pre-shifted by F.s
 };
 
-template <int K, int OP>
+template <int K, int OP, int STRAT>
 __global__ void __launch_bounds__(256) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
                                                    int64_t n, const __grid_constant__ BlasArgs<K> args) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -158,17 +158,17 @@ __global__ void __launch_bounds__(256) blas_kernel(const uint32_t *a, const uint
     } else if constexpr (OP == OP_VSUB) {
       sub_mod<K>(r, x, y, args.F.q);
     } else if constexpr (OP == OP_VMUL) {
-      mul_barrett<K>(r, x, y, args.F);
+      mul_barrett<K, STRAT>(r, x, y, args.F);
     } else {
       uint32_t t[K];
-      mul_barrett_pre<K>(t, args.scal, x, args.F);
+      mul_barrett_pre<K, barrett_style<K>(), STRAT>(t, args.scal, x, args.F);
       add_mod<K>(r, t, y, args.F.q);
     }
     store_elem<K>(out, i, r);
   }
 }
 
-template <int K, int OP>
+template <int K, int OP, int STRAT>
 static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out,
                        int64_t n, const uint32_t *scal_host, cudaStream_t st) {
   static int blocks_per_sm = -1;
@@ -178,7 +178,7 @@ static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, 
     WM_CUDA_TRY(cudaGetDevice(&dev));
     WM_CUDA_TRY(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
     int nb = 0;
-    WM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, blas_kernel<K, OP>, 256, 0));
+    WM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, blas_kernel<K, OP, STRAT>, 256, 0));
     blocks_per_sm = std::max(1, nb);
   }
   BlasArgs<K> args;
@@ -191,7 +191,7 @@ static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, 
   int64_t want = (n + 255) / 256;
   int64_t cap = (int64_t)sm_count * blocks_per_sm * 4;  // a few waves' worth of resident CTAs
   int grid = (int)std::max<int64_t>(1, std::min(want, cap));
-  blas_kernel<K, OP><<<grid, 256, 0, st>>>(a, b, out, n, args);
+  blas_kernel<K, OP, STRAT><<<grid, 256, 0, st>>>(a, b, out, n, args);
   WM_LAUNCH_CHECK("blas_kernel launch");
   return WM_OK;
 }
@@ -204,13 +204,17 @@ static int blas_dispatch(int op, const wm_field *f, const uint32_t *a, const uin
   if (!a || !b || !out) return fail(WM_EINVAL, "null data pointer");
   cudaStream_t st = (cudaStream_t)stream;
   switch (f->K) {
-#define WM_CASE(k)                                                                     \
-  case k:                                                                              \
-    switch (op) {                                                                      \
-      case OP_VADD: return launch_blas<k, OP_VADD>(f, a, b, out, n, nullptr, st);      \
-      case OP_VSUB: return launch_blas<k, OP_VSUB>(f, a, b, out, n, nullptr, st);      \
-      case OP_VMUL: return launch_blas<k, OP_VMUL>(f, a, b, out, n, nullptr, st);      \
-      default: return launch_blas<k, OP_AXPY>(f, a, b, out, n, scal_host, st);         \
+#define WM_CASE(k)                                                                                 \
+  case k:                                                                                          \
+    switch (op) {                                                                                  \
+      case OP_VADD: return launch_blas<k, OP_VADD, kSchoolbook>(f, a, b, out, n, nullptr, st);     \
+      case OP_VSUB: return launch_blas<k, OP_VSUB, kSchoolbook>(f, a, b, out, n, nullptr, st);     \
+      case OP_VMUL:                                                                                \
+        return f->karatsuba ? launch_blas<k, OP_VMUL, kKaratsuba>(f, a, b, out, n, nullptr, st)    \
+                            : launch_blas<k, OP_VMUL, kSchoolbook>(f, a, b, out, n, nullptr, st);  \
+      default:                                                                                     \
+        return f->karatsuba ? launch_blas<k, OP_AXPY, kKaratsuba>(f, a, b, out, n, scal_host, st)  \
+                            : launch_blas<k, OP_AXPY, kSchoolbook>(f, a, b, out, n, scal_host, st);\
     }
     WM_BLAS_KS(WM_CASE)
 #undef WM_CASE
@@ -286,6 +290,10 @@ int wm_supported_limbs(int ntt, int *out, int cap) {
 }
 
 int wm_field_create(int bits, const uint32_t *q_host, int q_limbs, wm_field **out) {
+  return wm_field_create_ex(bits, q_host, q_limbs, 0, out);
+}
+
+int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags, wm_field **out) {
   if (!out) return fail(WM_EINVAL, "null output pointer");
   *out = nullptr;
   if (bits < 8) return fail(WM_EINVAL, "width must be at least 8 bits");
@@ -302,7 +310,9 @@ int wm_field_create(int bits, const uint32_t *q_host, int q_limbs, wm_field **ou
   if (qb < 2) return fail(WM_EINVAL, "modulus must exceed 1");
   if (qb > M) return fail(WM_EINVAL, "modulus must be below 2^(32K-4)");
   if (M - qb > 31) return fail(WM_EINVAL, "modulus too small for the field width (normalisation shift > 31)");
+  if (flags & ~WM_FIELD_KARATSUBA) return fail(WM_EINVAL, "unknown field flags");
   wm_field *f = new wm_field();
+  f->karatsuba = (flags & WM_FIELD_KARATSUBA) != 0;
   f->bits = bits;
   f->K = K;
   f->s = M - qb;

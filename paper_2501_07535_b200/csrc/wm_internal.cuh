@@ -55,6 +55,7 @@ Big big_pow2_div(int e, const Big &d, int limbs);
 }  // namespace wm
 
 struct wm_field {
+  bool karatsuba = false;  // vmul/axpy use the Karatsuba full product
   int bits = 0;
   int K = 0;
   int s = 0;

@@ -312,6 +312,95 @@ WM_DEV void mul_lo_acc(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t 
 }
 
 
+// ------------------------------------------------------------------ Karatsuba
+// One Karatsuba level on a full K x K product (K even, H = K/2), the device
+// form of the reference's "karatsuba" mul_strategy (rewrite.py:234-253):
+//   z0 = a0 b0, z2 = a1 b1, z1 = (a0 + a1)(b0 + b1) - z0 - z2,
+//   t  = z0 + z1 B + z2 B^2           (B = 2^(32H))
+// with the carry bits of the half sums folded in by masked adds.  3H^2 word
+// products instead of 4H^2, recursing while the half is still >= 8 limbs.
+enum MulStrategy { kSchoolbook = 0, kKaratsuba = 1 };
+
+template <int K, int ST, int STRAT>
+WM_DEV void mul_full_s(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]);
+
+template <int K, int ST>
+WM_DEV void mul_full_kara(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  constexpr int H = K / 2;
+  constexpr int SUB = (H >= 8 && (H % 2) == 0) ? kKaratsuba : kSchoolbook;
+  uint32_t a0[H], a1[H], b0[H], b1[H];
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    a0[j] = a[j]; a1[j] = a[H + j];
+    b0[j] = b[j]; b1[j] = b[H + j];
+  }
+  uint32_t z0[2 * H], z2[2 * H], zm[2 * H];
+  mul_full_s<H, ST, SUB>(z0, a0, b0);
+  mul_full_s<H, ST, SUB>(z2, a1, b1);
+  uint32_t sa[H], sb[H];
+  const uint32_t ca = add_n<H>(sa, a0, a1);
+  const uint32_t cb = add_n<H>(sb, b0, b1);
+  mul_full_s<H, ST, SUB>(zm, sa, sb);
+  // z1 = zm + (ca ? sb : 0) B + (cb ? sa : 0) B + ca cb B^2  - z0 - z2   (2H+1 limbs)
+  uint32_t z1[2 * H + 1];
+#pragma unroll
+  for (int j = 0; j < 2 * H; ++j) z1[j] = zm[j];
+  z1[2 * H] = ca & cb;
+  {
+    const uint32_t ma = 0u - ca, mb = 0u - cb;
+    uint32_t hi[H + 1], x[H + 1], y[H + 1];
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      hi[j] = z1[H + j];
+      x[j] = sb[j] & ma;
+      y[j] = sa[j] & mb;
+    }
+    hi[H] = z1[2 * H];
+    x[H] = 0u;
+    y[H] = 0u;
+    add_n<H + 1>(hi, hi, x);
+    add_n<H + 1>(hi, hi, y);
+#pragma unroll
+    for (int j = 0; j <= H; ++j) z1[H + j] = hi[j];
+  }
+  {
+    uint32_t e0[2 * H + 1], e2[2 * H + 1];
+#pragma unroll
+    for (int j = 0; j < 2 * H; ++j) {
+      e0[j] = z0[j];
+      e2[j] = z2[j];
+    }
+    e0[2 * H] = 0u;
+    e2[2 * H] = 0u;
+    sub_n<2 * H + 1>(z1, z1, e0);
+    sub_n<2 * H + 1>(z1, z1, e2);
+  }
+  // t = z0 | z2 << 64H, then += z1 << 32H (carry ripples to the top)
+#pragma unroll
+  for (int j = 0; j < 2 * H; ++j) {
+    t[j] = z0[j];
+    t[2 * H + j] = z2[j];
+  }
+  uint32_t mid[3 * H], add[3 * H];
+#pragma unroll
+  for (int j = 0; j < 3 * H; ++j) {
+    mid[j] = t[H + j];
+    add[j] = (j <= 2 * H) ? z1[j] : 0u;
+  }
+  add_n<3 * H>(mid, mid, add);
+#pragma unroll
+  for (int j = 0; j < 3 * H; ++j) t[H + j] = mid[j];
+}
+
+template <int K, int ST, int STRAT>
+WM_DEV void mul_full_s(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  if constexpr (STRAT == kKaratsuba && (K % 2) == 0 && K >= 4) {
+    mul_full_kara<K, ST>(t, a, b);
+  } else {
+    mul_full<K, ST>(t, a, b);
+  }
+}
+
 // ------------------------------------------------------------------ Shoup
 // Multiply by a fixed operand w with precomputed wp = floor(w * 2^(32K) / p)
 // (Shoup / Harvey).  With np = 2^(32K) - p:
@@ -449,7 +538,7 @@ WM_DEV void shr_small(uint32_t (&r)[K], const uint32_t (&a)[K], uint32_t s) {
 // Default multiplier style for the Barrett path per limb count (A/B:
 // tools/ab_timing.py; WM_BARRETT_FORCE=0/1 overrides for experiments).
 template <int K>
-constexpr int barrett_style() {
+__host__ __device__ constexpr int barrett_style() {
 #if defined(WM_BARRETT_FORCE)
   return WM_BARRETT_FORCE;
 #else
@@ -457,11 +546,11 @@ constexpr int barrett_style() {
 #endif
 }
 
-template <int K, int ST = barrett_style<K>()>
+template <int K, int ST = barrett_style<K>(), int STRAT = kSchoolbook>
 WM_DEV void mul_barrett_pre(uint32_t (&r)[K], const uint32_t (&a_shifted)[K], const uint32_t (&b)[K],
                             const FieldConst<K> &F) {
   uint32_t t[2 * K];
-  mul_full<K, ST>(t, a_shifted, b);
+  mul_full_s<K, ST, STRAT>(t, a_shifted, b);
   // q1 = t >> (M - 1) = t >> (32K - 5): limbs K-1 .. 2K-1 shifted by 27.
   uint32_t q1[K];
 #pragma unroll
@@ -477,12 +566,12 @@ WM_DEV void mul_barrett_pre(uint32_t (&r)[K], const uint32_t (&a_shifted)[K], co
   shr_small<K>(r, rr, F.s);
 }
 
-template <int K>
+template <int K, int STRAT = kSchoolbook>
 WM_DEV void mul_barrett(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K],
                         const FieldConst<K> &F) {
   uint32_t as[K];
   shl_small<K>(as, a, F.s);
-  mul_barrett_pre<K>(r, as, b, F);
+  mul_barrett_pre<K, barrett_style<K>(), STRAT>(r, as, b, F);
 }
 
 }  // namespace wm

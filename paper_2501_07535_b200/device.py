@@ -85,18 +85,22 @@ class Field:
     (C ABI ``wm_field_*``).  Replaces the baked q/mu of a generated reference
     kernel (kernels._param_vars, kernels.py:168-181)."""
 
-    def __init__(self, bits: int, q: int):
+    def __init__(self, bits: int, q: int, strategy: str = "schoolbook"):
         self.lib = _lib.load()
         self.bits = int(bits)
         self.q = int(q)
+        if strategy not in ("schoolbook", "karatsuba"):
+            raise ValueError(f"unknown multiplication strategy {strategy!r}")
+        self.strategy = strategy
         self.limbs = limbs_for_bits(self.bits)
         if self.q <= 1:
             raise ValueError(f"modulus must exceed 1, got {q}")
         ql = ints_to_limbs([self.q], self.limbs)[0]
         arr = _lib.u32_array(ql.tolist())
         h = ctypes.c_void_p()
-        _lib.check(self.lib.wm_field_create(self.bits, arr, self.limbs, ctypes.byref(h)),
-                   "wm_field_create")
+        flags = 1 if strategy == "karatsuba" else 0
+        _lib.check(self.lib.wm_field_create_ex(self.bits, arr, self.limbs, flags, ctypes.byref(h)),
+                   "wm_field_create_ex")
         self._h = h
         b, k, s = _i(), _i(), _i()
         _lib.check(self.lib.wm_field_info(self._h, ctypes.byref(b), ctypes.byref(k), ctypes.byref(s)))

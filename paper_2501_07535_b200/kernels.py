@@ -124,13 +124,13 @@ _fields: dict = {}
 _plans: dict = {}
 
 
-def get_field(bits: int, q: int) -> Field:
-    """Shared device field for (width, modulus)."""
-    key = (bits, q)
+def get_field(bits: int, q: int, strategy: str = "schoolbook") -> Field:
+    """Shared device field for (width, modulus, multiplication strategy)."""
+    key = (bits, q, strategy)
     with _cache_lock:
         f = _fields.get(key)
         if f is None:
-            f = Field(bits, q)
+            f = Field(bits, q, strategy)
             _fields[key] = f
         return f
 
@@ -223,7 +223,10 @@ class DeviceKernel:
         return self.spec.ntt.p if self.spec.ntt is not None else self.spec.barrett.q
 
     def field(self) -> Field:
-        return get_field(self.spec.layout.bits, self.modulus)
+        """Device field; the spec's mul_strategy ("schoolbook"/"karatsuba",
+        reference KernelSpec.mul_strategy) selects the vmul/axpy multiplier."""
+        strat = self.spec.mul_strategy if self.spec.mul_strategy in ("schoolbook", "karatsuba") else "schoolbook"
+        return get_field(self.spec.layout.bits, self.modulus, strat)
 
     def plan(self) -> NttPlan:
         if self.spec.ntt is None:

@@ -22,9 +22,9 @@ def _dev():
     return device
 
 
-def run_op(kind, bits, q, xs, ys, scalar=0):
+def run_op(kind, bits, q, xs, ys, scalar=0, strategy="schoolbook"):
     dev = _dev()
-    f = dev.Field(bits, q)
+    f = dev.Field(bits, q, strategy)
     x = dev.to_device(dev.ints_to_limbs(xs, f.limbs))
     y = dev.to_device(dev.ints_to_limbs(ys, f.limbs))
     out = f.axpy(scalar, x, y) if kind == "axpy" else getattr(f, kind)(x, y)
@@ -58,10 +58,13 @@ def test_golden_vectors(cuda, golden):
         assert got == [int(v) for v in row["out"]], (row["kind"], row["bits"])
 
 
-def test_api_run_vector_matches_reference_goldens(cuda, golden):
+@pytest.mark.parametrize("strategy", ["schoolbook", "karatsuba"])
+def test_api_run_vector_matches_reference_goldens(cuda, golden, strategy):
+    """Through the reference-mirroring API, incl. make_spec(strategy=...)
+    (reference kernels.py:104-117)."""
     from paper_2501_07535_b200 import kernels as K
-    for row in golden("blas")[:8]:
-        spec = K.make_spec(row["kind"], row["bits"], row["word"], size=len(row["a"]))
+    for row in golden("blas"):
+        spec = K.make_spec(row["kind"], row["bits"], row["word"], size=len(row["a"]), strategy=strategy)
         prog = K.generate_kernel(spec)
         xs = [int(v) for v in row["a"]]
         ys = [int(v) for v in row["b"]]
@@ -70,7 +73,7 @@ def test_api_run_vector_matches_reference_goldens(cuda, golden):
 
 
 @pytest.mark.parametrize("bits", WIDTHS)
-@pytest.mark.parametrize("kind", ["vadd", "vsub", "vmul", "axpy"])
+@pytest.mark.parametrize("kind", ["vadd", "vsub", "vmul", "axpy", "vmul_karatsuba", "axpy_karatsuba"])
 def test_random_and_edges_vs_oracle(cuda, bits, kind):
     """Reference moduli (largest prime below 2^(bits-4)) and a random general
     modulus in the Barrett range; seeded inputs plus the {0,1,q-1}^2 grid."""
@@ -88,7 +91,9 @@ def test_random_and_edges_vs_oracle(cuda, bits, kind):
         xs += [a for a in edge for _ in edge]
         ys += [b for _ in edge for b in edge]
         s = rnd.randrange(q)
-        got = run_op(kind, bits, q, xs, ys, s)
+        op, _, strat = kind.partition("_")
+        got = run_op(op, bits, q, xs, ys, s, strat or "schoolbook")
+        kind = op
         if kind == "vadd":
             want = [(a + b) % q for a, b in zip(xs, ys)]
         elif kind == "vsub":
@@ -100,17 +105,18 @@ def test_random_and_edges_vs_oracle(cuda, bits, kind):
         assert got == want, (kind, bits, q)
 
 
-def test_adversarial_vmul_operands(cuda):
+@pytest.mark.parametrize("strategy", ["schoolbook", "karatsuba"])
+def test_adversarial_vmul_operands(cuda, strategy):
     """Operands that maximise the Barrett quotient error: q-1, q-2, values
     near powers of two, and all-ones limbs below q."""
     from paper_2501_07535_b200.params import find_ntt_params
-    for bits in (64, 128, 256, 384, 768):
+    for bits in (64, 128, 256, 384, 512, 768, 1024):
         q = find_ntt_params(bits, 1).p
         specials = [q - 1, q - 2, (q - 1) // 2, (q + 1) // 2, 1 << (bits - 5), (1 << (bits - 5)) - 1,
                     q - (1 << 32), (1 << 32) - 1, 2, 3]
         xs = [a for a in specials for _ in specials]
         ys = [b for _ in specials for b in specials]
-        assert run_op("vmul", bits, q, xs, ys) == [a * b % q for a, b in zip(xs, ys)]
+        assert run_op("vmul", bits, q, xs, ys, 0, strategy) == [a * b % q for a, b in zip(xs, ys)]
 
 
 def test_aliasing_and_sizes(cuda):

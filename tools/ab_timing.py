@@ -27,12 +27,13 @@ assert torch.equal(z, x)
 res = {"ntt_step_ms": ms, "us_per_transform": ms * 1e3 / 128}
 for bits in (128, 256, 384, 768):
     Kl = bits // 32
-    f = dev.Field(bits, find_ntt_params(bits, 1).p)
     n = 1 << 22
     a = torch.randint(0, 1 << 27, (n, Kl), dtype=torch.int32, device="cuda"); b = a.flip(0).contiguous()
     o = torch.empty_like(a)
-    mv = t(lambda: f.vmul(a, b, out=o))
-    res[f"vmul{bits}_GBps"] = round(3 * 4 * Kl * n / mv / 1e6, 1)
+    for strat in ("schoolbook", "karatsuba"):
+        f = dev.Field(bits, find_ntt_params(bits, 1).p, strat)
+        mv = t(lambda: f.vmul(a, b, out=o))
+        res[f"vmul{bits}_{strat[:4]}_GBps"] = round(3 * 4 * Kl * n / mv / 1e6, 1)
 print(json.dumps(res))
 ''' % str(ROOT)
 for lib in sys.argv[1:]:
