@@ -305,9 +305,12 @@ def run_blas(args, torch, _field, pg):
         a[:, K - 1] &= top
         b[:, K - 1] &= top
         out = torch.empty_like(a)
+        # multiplier strategy per width: Karatsuba wins from 12 limbs up (tools/ab_timing.py)
+        fk = dev.Field(bits, q, "karatsuba") if K >= 12 else f
         for op in ("vadd", "vmul", "axpy"):
-            fn = (lambda: f.axpy(123456789, a, b, out=out)) if op == "axpy" else \
-                (lambda op=op: getattr(f, op)(a, b, out=out))
+            fm = fk if op in ("vmul", "axpy") else f
+            fn = (lambda: fm.axpy(123456789, a, b, out=out)) if op == "axpy" else \
+                (lambda op=op, fm=fm: getattr(fm, op)(a, b, out=out))
             for _ in range(3):
                 fn()
             torch.cuda.synchronize()
@@ -320,7 +323,7 @@ def run_blas(args, torch, _field, pg):
             ms = statistics.median(x.elapsed_time(y) for x, y in evs)
             gbs = 3 * 4 * K * n / (ms * 1e-3) / 1e9
             out_rows.append({"op": op, "bits": bits, "n": n, "ms": round(ms, 4), "GB_per_s": round(gbs, 1),
-                             "hbm_frac_of_measured": round(gbs / hbm, 3)})
+                             "hbm_frac_of_measured": round(gbs / hbm, 3), "strategy": fm.strategy})
         del a, b, out
     return {"rows": out_rows, "hbm_measured_gbs": hbm,
             "note": "median of 10 launches; operands 0.8-4.8 GB (> L2); bytes = 2 reads + 1 write per element"}
