@@ -75,7 +75,7 @@ struct wm_pass_plan {
   int64_t C1 = 0, C2 = 0, C3 = 0;
   bool scaled_table = false;  // inverse: use the n^-1-scaled table for this pass
   bool scale_out = false;     // inverse one-pass plans: multiply outputs by n^-1
-  bool canonical_out = false; // last pass of the transform: [0, 4p) -> [0, p)
+  bool canonical_out = false; // last pass of the transform: [0, 6p) -> [0, p)
   int src = 0, dst = 0;       // 0 = user in/out, 1 = workspace (see plan creation)
 };
 
@@ -87,7 +87,7 @@ struct wm_ntt_plan {
   std::vector<wm_pass_plan> passes;
   // device tables: n entries of (w, w') pairs (2K words each)
   uint32_t *tw_fwd = nullptr, *tw_inv = nullptr, *tw_inv_scaled = nullptr;
-  wm::Big ninv, ninv_sh, np, p2;  // n^-1, floor(n^-1 * 2^32K / p), 2^32K - p, 2p
+  wm::Big ninv, ninv_sh, np, p2, p3, p4;  // n^-1, floor(n^-1 * 2^32K / p), 2^32K - p, 2p, 3p, 4p
   // internal workspace (used when the caller passes none)
   std::mutex ws_mu;
   void *ws = nullptr;

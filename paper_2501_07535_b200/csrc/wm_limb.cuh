@@ -433,44 +433,45 @@ WM_DEV void mul_shoup(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (
 }
 
 // ------------------------------------------------------------------ lazy butterflies
-// Harvey-style lazy reduction for the NTT: values live in [0, 4p) between
-// stages and passes (4p < 2^(32K) because p < 2^(32K-4)); only the last pass
-// of a transform makes them canonical.
-//   t  = shoup_lazy(v)            in [0, 3p)  -> cond_sub p   -> [0, 2p)
-//   u  = cond_sub(u, 2p)          in [0, 2p)
-//   x0 = u + t                    in [0, 4p)
-//   x1 = (u + 2p) - t             in (0, 4p)
+// Lazy reduction for the NTT (after Harvey): values live in [0, 6p) between
+// stages and passes (6p < 2^(32K) because p < 2^(32K-4)); only the last pass
+// makes them canonical.  The truncated Shoup product is in [0, 3p), so
+//   u  = cond_sub(u, 3p)          in [0, 3p)
+//   x0 = u + t                    in [0, 6p)
+//   x1 = (u + 3p) - t             in (0, 6p)
+// costs one conditional subtraction per butterfly (a [0, 4p) window would
+// need a second one on t).
 template <int K>
-WM_DEV void bf_finish(uint32_t (&x0)[K], uint32_t (&x1)[K], uint32_t (&t)[K], const uint32_t (&p2)[K]) {
+WM_DEV void bf_finish(uint32_t (&x0)[K], uint32_t (&x1)[K], uint32_t (&t)[K], const uint32_t (&p3)[K]) {
   uint32_t u[K], a[K];
   copy_n<K>(u, x0);
-  cond_sub<K>(u, p2);
+  cond_sub<K>(u, p3);
   add_n<K>(x0, u, t);
-  add_n<K>(a, u, p2);
+  add_n<K>(a, u, p3);
   sub_n<K>(x1, a, t);
 }
 
 template <int K>
 WM_DEV void bf_lazy(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&wp)[K],
-                    const uint32_t (&p)[K], const uint32_t (&p2)[K], const uint32_t (&np)[K]) {
+                    const uint32_t (&p3)[K], const uint32_t (&np)[K]) {
   uint32_t t[K];
   mul_shoup_lazy<K>(t, x1, w, wp, np);
-  cond_sub<K>(t, p);
-  bf_finish<K>(x0, x1, t, p2);
+  bf_finish<K>(x0, x1, t, p3);
 }
 
-// Butterfly with twiddle 1 (stage 0): t = v reduced from [0, 4p) to [0, 2p).
+// Butterfly with twiddle 1 (stage 0): t = v reduced from [0, 6p) to [0, 3p).
 template <int K>
-WM_DEV void bf_lazy_w1(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&p2)[K]) {
+WM_DEV void bf_lazy_w1(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&p3)[K]) {
   uint32_t t[K];
   copy_n<K>(t, x1);
-  cond_sub<K>(t, p2);
-  bf_finish<K>(x0, x1, t, p2);
+  cond_sub<K>(t, p3);
+  bf_finish<K>(x0, x1, t, p3);
 }
 
-// [0, 4p) -> [0, p)
+// [0, 6p) -> [0, p)
 template <int K>
-WM_DEV void canonical_4p(uint32_t (&x)[K], const uint32_t (&p)[K], const uint32_t (&p2)[K]) {
+WM_DEV void canonical_6p(uint32_t (&x)[K], const uint32_t (&p)[K], const uint32_t (&p2)[K], const uint32_t (&p4)[K]) {
+  cond_sub<K>(x, p4);
   cond_sub<K>(x, p2);
   cond_sub<K>(x, p);
 }

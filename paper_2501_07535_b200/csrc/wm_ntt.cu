@@ -49,6 +49,8 @@ struct NttConst {
   FieldConst<K> F;  // Barrett constants of p (pointwise-product epilogue)
   uint32_t p[K];
   uint32_t p2[K];   // 2p
+  uint32_t p3[K];   // 3p (lazy window)
+  uint32_t p4[K];   // 4p
   uint32_t np[K];   // 2^(32K) - p
   uint32_t sc[K];   // n^-1            (one-pass inverse epilogue)
   uint32_t scp[K];  // its Shoup companion
@@ -126,28 +128,28 @@ __device__ __forceinline__ void radix4_single(uint32_t (&x0)[K], uint32_t (&x1)[
   using S = Smem<K>;
   uint32_t w[K], wp[K];
   if (s == 0) {
-    bf_lazy_w1<K>(x0, x1, c.p2);
-    bf_lazy_w1<K>(x2, x3, c.p2);
-    bf_lazy_w1<K>(x0, x2, c.p2);  // j = 0: root^0
+    bf_lazy_w1<K>(x0, x1, c.p3);
+    bf_lazy_w1<K>(x2, x3, c.p3);
+    bf_lazy_w1<K>(x0, x2, c.p3);  // j = 0: root^0
   } else {
     const int i1 = j << (logL - 1 - s);
     S::load(w, tww, i1);
     S::load(wp, twp, i1);
-    bf_lazy<K>(x0, x1, w, wp, c.p, c.p2, c.np);
-    bf_lazy<K>(x2, x3, w, wp, c.p, c.p2, c.np);
+    bf_lazy<K>(x0, x1, w, wp, c.p3, c.np);
+    bf_lazy<K>(x2, x3, w, wp, c.p3, c.np);
     const int i2 = j << (lq - s);
     S::load(w, tww, i2);
     S::load(wp, twp, i2);
-    bf_lazy<K>(x0, x2, w, wp, c.p, c.p2, c.np);
+    bf_lazy<K>(x0, x2, w, wp, c.p3, c.np);
   }
   const int i3 = (j + h) << (lq - s);
   S::load(w, tww, i3);
   S::load(wp, twp, i3);
-  bf_lazy<K>(x1, x3, w, wp, c.p, c.p2, c.np);
+  bf_lazy<K>(x1, x3, w, wp, c.p3, c.np);
 }
 
 // G lines of L = 2^logL elements (tile element g*L + pos), bit-reversed order
-// on entry, natural order on exit, values in [0, 4p) throughout.  Stages run
+// on entry, natural order on exit, values in [0, 6p) throughout.  Stages run
 // two at a time as radix-4 groups held in registers (one shared-memory round
 // trip and one barrier per two stages); an odd leading stage runs radix-2.
 // tww/twp[e] (e < L/2) = root_L^e and its Shoup companion.
@@ -168,13 +170,13 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
       S::load(x0, data, e0);
       S::load(x1, data, e0 + h);
       if (s == 0) {
-        bf_lazy_w1<K>(x0, x1, c.p2);
+        bf_lazy_w1<K>(x0, x1, c.p3);
       } else {
         uint32_t w[K], wp[K];
         const int i1 = j << (logL - 1 - s);
         S::load(w, tww, i1);
         S::load(wp, twp, i1);
-        bf_lazy<K>(x0, x1, w, wp, c.p, c.p2, c.np);
+        bf_lazy<K>(x0, x1, w, wp, c.p3, c.np);
       }
       S::store(data, e0, x0);
       S::store(data, e0 + h, x1);
@@ -190,7 +192,7 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
       uint32_t x0[K], x1[K];
       S::load(x0, data, e0);
       S::load(x1, data, e0 + 1);
-      bf_lazy_w1<K>(x0, x1, c.p2);
+      bf_lazy_w1<K>(x0, x1, c.p3);
       S::store(data, e0, x0);
       S::store(data, e0 + 1, x1);
     }
@@ -281,7 +283,7 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass
       mul_shoup_lazy<K>(r, v, w, wp, c.np);
       copy_n<K>(v, r);
     }
-    if (d.canonical_out) canonical_4p<K>(v, c.p, c.p2);
+    if (d.canonical_out) canonical_6p<K>(v, c.p, c.p2, c.p4);
     const int64_t pos = base + o * d.WO + (int64_t)k * d.WK + i0 + g;
     if (d.mul_by) {
       uint32_t m[K], rr[K];
@@ -334,7 +336,7 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass
         mul_shoup_lazy<K>(rr, v, c.sc, c.scp, c.np);
         copy_n<K>(v, rr);
       }
-      if (d.canonical_out) canonical_4p<K>(v, c.p, c.p2);
+      if (d.canonical_out) canonical_6p<K>(v, c.p, c.p2, c.p4);
       const int64_t pos = b * d.n + r * d.WO + (int64_t)k * d.WK;
       if (d.mul_by) {  // fused pointwise product (NTT-domain convolution)
         uint32_t m[K], rr[K];
@@ -433,6 +435,8 @@ static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
   for (int j = 0; j < K; ++j) {
     c.p[j] = pl->field->q[j];
     c.p2[j] = pl->p2[j];
+    c.p3[j] = pl->p3[j];
+    c.p4[j] = pl->p4[j];
     c.np[j] = pl->np[j];
     c.sc[j] = pl->ninv[j];
     c.scp[j] = pl->ninv_sh[j];
@@ -686,6 +690,9 @@ int wm_ntt_plan_create(const wm_field *f, int64_t n, const uint32_t *root_host, 
     pl->np = Big(K, 0u);
     big_sub_inplace(pl->np, f->q);
     pl->p2 = big_shl(f->q, 1, K);
+    pl->p4 = big_shl(f->q, 2, K);
+    pl->p3 = pl->p4;
+    big_sub_inplace(pl->p3, f->q);
   }
   int rc = plan_passes(pl);
   if (rc) {
