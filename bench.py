@@ -292,6 +292,7 @@ def run_blas(args, torch, _field, pg):
     from paper_2501_07535_b200.params import find_ntt_params
     n = 1 << 24
     hbm = peaks().get("hbm_gbs", 6650.0)
+    int_peak, _ = int_peak_wmul_per_s(None)
     out_rows = []
     stream = torch.cuda.current_stream()
     for bits in args.blas_bits:
@@ -322,11 +323,18 @@ def run_blas(args, torch, _field, pg):
             torch.cuda.synchronize()
             ms = statistics.median(x.elapsed_time(y) for x, y in evs)
             gbs = 3 * 4 * K * n / (ms * 1e-3) / 1e9
+            # binding roofline: max(HBM time, integer time of the
+            # reference's 3k^2 word products per element) over the measured time
+            t_hbm = 3 * 4 * K * n / (hbm * 1e9)
+            t_int = (3 * K * K * n / int_peak) if op in ("vmul", "axpy") else 0.0
+            bound = "int" if t_int > t_hbm else "hbm"
             out_rows.append({"op": op, "bits": bits, "n": n, "ms": round(ms, 4), "GB_per_s": round(gbs, 1),
-                             "hbm_frac_of_measured": round(gbs / hbm, 3), "strategy": fm.strategy})
+                             "hbm_frac_of_measured": round(gbs / hbm, 3), "strategy": fm.strategy,
+                             "binding": bound, "binding_frac": round(max(t_hbm, t_int) / (ms * 1e-3), 3)})
         del a, b, out
-    return {"rows": out_rows, "hbm_measured_gbs": hbm,
-            "note": "median of 10 launches; operands 0.8-4.8 GB (> L2); bytes = 2 reads + 1 write per element"}
+    return {"rows": out_rows, "hbm_measured_gbs": hbm, "int_peak_twmul_s": round(int_peak / 1e12, 3),
+            "note": "median of 10 launches; operands 0.8-4.8 GB (> L2); bytes = 2 reads + 1 write per element; "
+                    "binding_frac = max(bytes/HBM, 3k^2 products/int peak) / measured time"}
 
 
 def run_four_step(args, torch, rank, world, pg):
@@ -359,9 +367,30 @@ def run_four_step(args, torch, rank, world, pg):
     torch.cuda.synchronize()
     ms = max_over_ranks(pg, e0.elapsed_time(e1) / reps)
     a2a_bytes = (world - 1) * (n // world) * 4 * K_LIMBS // world
-    return {"n": n, "ranks": world, "ms_per_forward": round(ms, 4), "us_per_transform": round(ms * 1e3, 2),
-            "split": [L.n1, L.n2], "a2a_bytes_sent_per_rank": a2a_bytes,
-            "note": "max over ranks; forward only; input rows j1 per rank (scatter not timed)"}
+    res = {"n": n, "ranks": world, "ms_per_forward": round(ms, 4), "us_per_transform": round(ms * 1e3, 2),
+           "split": [L.n1, L.n2], "a2a_bytes_sent_per_rank": a2a_bytes,
+           "note": "max over ranks; forward only; input rows j1 per rank (scatter not timed)"}
+    del eng, x, y, back
+    if world == 1:
+        # the same transform through the single-GPU multi-pass plan (natural order in/out)
+        from paper_2501_07535_b200 import kernels as K
+        plan = K.get_plan(BITS, prm)
+        xs = canonical_random(torch, n, 4343)
+        ys = torch.empty_like(xs)
+        ws = torch.empty(max(1, plan.workspace_bytes(1) // 4), dtype=torch.int32, device="cuda")
+        for _ in range(2):
+            plan.forward(xs, out=ys, workspace=ws)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            plan.forward(xs, out=ys, workspace=ws)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        res["single_gpu_plan_ms_per_forward"] = round(e0.elapsed_time(e1) / reps, 4)
+        res["single_gpu_plan_passes"] = plan.pass_log_sizes
+        del xs, ys, ws
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_batched_2p20(args, torch, rank, world, pg):

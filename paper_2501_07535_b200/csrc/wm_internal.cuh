@@ -87,6 +87,12 @@ struct wm_ntt_plan {
   std::vector<wm_pass_plan> passes;
   // device tables: n entries of (w, w') pairs (2K words each)
   uint32_t *tw_fwd = nullptr, *tw_inv = nullptr, *tw_inv_scaled = nullptr;
+  // per-pass twiddle sub-tables as shared-memory images (TMA bulk-copied by the
+  // pass kernels): forward images at tw_img + tw_img_off[pass], inverse images
+  // tw_img_words_dir words further
+  uint32_t *tw_img = nullptr;
+  std::vector<size_t> tw_img_off;
+  size_t tw_img_words_dir = 0;
   wm::Big ninv, ninv_sh, np, p2, p3, p4;  // n^-1, floor(n^-1 * 2^32K / p), 2^32K - p, 2p, 3p, 4p
   // internal workspace (used when the caller passes none)
   std::mutex ws_mu;

@@ -69,6 +69,7 @@ struct PassDesc {
   int64_t tw_stride;  // n / L
   int64_t total_lines;  // row passes: batch * lines_inner
   const uint32_t *mul_by;  // last pass: out[pos] = result[pos] * mul_by[pos] mod p (convolution)
+  const uint32_t *tw_img;  // this pass's twiddle sub-table, pre-swizzled shared-memory image
 };
 
 // ------------------------------------------------------------------ smem layout
@@ -212,7 +213,6 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
       S::load(x1, data, e0 + h);
       S::load(x2, data, e0 + 2 * h);
       S::load(x3, data, e0 + 3 * h);
-      uint32_t w[K], wp[K];
       radix4_single<K>(x0, x1, x2, x3, tww, twp, s, j, h, logL, lq, c);
 
       S::store(data, e0, x0);
@@ -224,27 +224,69 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
   }
 }
 
+// Shared-memory map of a pass CTA (all offsets 16-byte aligned):
+//   [data tile: G*L elements][twiddle image: L/2 (w) + L/2 (w') elements][mbarrier]
+WM_DEV size_t round4(size_t words) { return (words + 3) & ~(size_t)3; }
 template <int K>
-__device__ __forceinline__ void load_subtw(uint32_t *tww, uint32_t *twp, const uint32_t *table, int logL,
-                                           int64_t stride) {
-  const int half = 1 << (logL - 1);
-  for (int idx = threadIdx.x; idx < half * 2; idx += blockDim.x) {
-    const int e = idx >> 1, part = idx & 1;
-    uint32_t v[K];
-    ldg_elem<K>(v, table + ((int64_t)e * stride) * (2 * K) + part * K);
-    Smem<K>::store(part ? twp : tww, e, v);
+WM_DEV size_t tile_words(int logL, int G) {
+  return round4((size_t)G * ((size_t)1 << logL) * K);
+}
+template <int K>
+WM_DEV size_t twimg_words(int logL) {
+  return round4(((size_t)1 << logL) * K);
+}
+
+// The pass's twiddle sub-table (root_L^e and its Shoup companion, e < L/2)
+// is precomputed at plan creation as the exact byte image of its swizzled
+// shared-memory layout, so one TMA bulk copy (cp.async.bulk, completion
+// counted on an mbarrier) stages it while the threads load the data tile.
+WM_DEV uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+WM_DEV void twimg_issue(uint32_t *dst, const uint32_t *src, uint32_t bytes, uint64_t *mbar) {
+  if (threadIdx.x == 0) {
+    const uint32_t mb = smem_addr(mbar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mb) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(mb)
+                 : "memory");
   }
 }
 
+// Every thread waits for phase 0 of the mbarrier (call after a __syncthreads
+// that follows twimg_issue, so the barrier is initialised).
+WM_DEV void twimg_wait(uint64_t *mbar) {
+  const uint32_t mb = smem_addr(mbar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(mb)
+        : "memory");
+  }
+}
+
+// Plan-time builder of a pass's twiddle image (same layout the pass reads).
 template <int K>
-__device__ __forceinline__ size_t tile_words(int logL, int G) {
-  return (size_t)G * ((size_t)1 << logL) * K;
+__global__ void twiddle_image_kernel(const uint32_t *table, int64_t stride, int logL, uint32_t *img) {
+  const int half = 1 << (logL - 1);
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < 2 * half; idx += gridDim.x * blockDim.x) {
+    const int e = idx >> 1, part = idx & 1;
+    uint32_t v[K];
+    ldg_elem<K>(v, table + ((int64_t)e * stride) * (2 * K) + part * K);
+    Smem<K>::store(img + (size_t)part * half * K, e, v);
+  }
 }
 
 // ------------------------------------------------------------------ column pass
 // Line (o, i), i in [0, lines_inner) consecutive per CTA (G of them).
 template <int K>
-__global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
+__global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass(const uint32_t *in, uint32_t *out,
                                                     const uint32_t *tw_out, const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -253,13 +295,14 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass
   uint32_t *data = smem;
   uint32_t *tww = smem + tile_words<K>(logL, G);
   uint32_t *twp = tww + (size_t)(L / 2) * K;
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(tww + twimg_words<K>(logL));
   const int64_t tiles_inner = d.lines_inner / G;
   const int64_t tile = blockIdx.x;
   const int64_t o = tile / tiles_inner;
   const int64_t i0 = (tile - o * tiles_inner) * G;
   const int64_t base = (int64_t)blockIdx.y * d.n;
 
-  load_subtw<K>(tww, twp, tw_sub, logL, d.tw_stride);
+  twimg_issue(tww, d.tw_img, (uint32_t)(twimg_words<K>(logL) * 4), mbar);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
     const int t = idx / G, g = idx - t * G;
     const int64_t pos = base + o * d.RO + (int64_t)t * d.RT + i0 + g;
@@ -269,6 +312,7 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass
     S::store(data, g * L + tb, v);
   }
   __syncthreads();
+  twimg_wait(mbar);
   dft_smem<K>(data, tww, twp, logL, G, c);
   const int64_t nmask = d.n - 1;
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
@@ -298,7 +342,7 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass
 // ------------------------------------------------------------------ row pass
 // Line lambda in [0, batch * lines_inner): b = lambda / R, r = lambda % R.
 template <int K>
-__global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass(const uint32_t *in, uint32_t *out, const uint32_t *tw_sub,
+__global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass(const uint32_t *in, uint32_t *out,
                                                     const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -307,9 +351,10 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass
   uint32_t *data = smem;
   uint32_t *tww = smem + tile_words<K>(logL, G);
   uint32_t *twp = tww + (size_t)(L / 2) * K;
+  uint64_t *mbar = reinterpret_cast<uint64_t *>(tww + twimg_words<K>(logL));
   const int64_t lam0 = (int64_t)blockIdx.x * G;
 
-  load_subtw<K>(tww, twp, tw_sub, logL, d.tw_stride);
+  twimg_issue(tww, d.tw_img, (uint32_t)(twimg_words<K>(logL) * 4), mbar);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
     const int g = idx >> logL, t = idx & (L - 1);
     const int64_t lam = lam0 + g;
@@ -323,6 +368,7 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass
     }
   }
   __syncthreads();
+  twimg_wait(mbar);
   dft_smem<K>(data, tww, twp, logL, G, c);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
     const int g = idx >> logL, k = idx & (L - 1);
@@ -444,9 +490,11 @@ static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
   return c;
 }
 
+static size_t round4_h(size_t w) { return (w + 3) & ~(size_t)3; }
+static size_t twimg_bytes(int K, int logL) { return round4_h(((size_t)1 << logL) * K) * sizeof(uint32_t); }
 static size_t pass_smem(int K, const wm_pass_plan &ps) {
   const size_t L = (size_t)1 << ps.logL;
-  return ((size_t)ps.G * L * K + (L / 2) * 2 * (size_t)K) * sizeof(uint32_t);
+  return round4_h((size_t)ps.G * L * K) * sizeof(uint32_t) + twimg_bytes(K, ps.logL) + 16;  // + mbarrier
 }
 
 template <int K>
@@ -460,7 +508,6 @@ static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, u
     attr_done = true;
   }
   const NttConst<K> c = ntt_const<K>(pl);
-  const uint32_t *tw_sub = inverse ? pl->tw_inv : pl->tw_fwd;
   for (int pi = 0; pi < (int)pl->passes.size(); ++pi) {
     if (only_pass >= 0 && pi != only_pass) continue;
     const wm_pass_plan &ps = pl->passes[pi];
@@ -489,16 +536,17 @@ static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, u
     d.tw_stride = pl->n >> ps.logL;
     d.total_lines = batch * ps.lines_inner;
     d.mul_by = (pi + 1 == (int)pl->passes.size()) ? mul_by : nullptr;
+    d.tw_img = pl->tw_img + (size_t)(inverse ? 1 : 0) * pl->tw_img_words_dir + pl->tw_img_off[pi];
     const size_t smem = pass_smem(K, ps);
     if (ps.column) {
       const uint32_t *tw_out = inverse ? (ps.scaled_table ? pl->tw_inv_scaled : pl->tw_inv) : pl->tw_fwd;
       dim3 grid((unsigned)(ps.lines_outer * (ps.lines_inner / ps.G)), (unsigned)batch);
-      ntt_col_pass<K><<<grid, 256, smem, st>>>(src, dst, tw_sub, tw_out, d, c);
+      ntt_col_pass<K><<<grid, 256, smem, st>>>(src, dst, tw_out, d, c);
       WM_LAUNCH_CHECK("ntt_col_pass launch");
     } else {
       const int64_t lines = batch * ps.lines_inner;
       dim3 grid((unsigned)((lines + ps.G - 1) / ps.G));
-      ntt_row_pass<K><<<grid, 256, smem, st>>>(src, dst, tw_sub, d, c);
+      ntt_row_pass<K><<<grid, 256, smem, st>>>(src, dst, d, c);
       WM_LAUNCH_CHECK("ntt_row_pass launch");
     }
   }
@@ -641,6 +689,26 @@ static int create_tables(wm_ntt_plan *pl, const Big &root, const Big &root_inv) 
     rc = gen_table<K>(pl->field, pl->tw_inv_scaled, n, root_inv, pl->ninv);
     if (rc) return rc;
   }
+  // per-pass twiddle images (forward block, then inverse block)
+  size_t words = 0;
+  pl->tw_img_off.clear();
+  for (const auto &ps : pl->passes) {
+    pl->tw_img_off.push_back(words);
+    words += twimg_bytes(K, ps.logL) / sizeof(uint32_t);
+  }
+  pl->tw_img_words_dir = words;
+  WM_CUDA_TRY(cudaMalloc(&pl->tw_img, 2 * words * sizeof(uint32_t)));
+  WM_CUDA_TRY(cudaMemset(pl->tw_img, 0, 2 * words * sizeof(uint32_t)));
+  for (int dir = 0; dir < 2; ++dir) {
+    const uint32_t *table = dir ? pl->tw_inv : pl->tw_fwd;
+    for (size_t pi = 0; pi < pl->passes.size(); ++pi) {
+      const int logL = pl->passes[pi].logL;
+      const int half = 1 << (logL - 1);
+      twiddle_image_kernel<K><<<(2 * half + 255) / 256, 256>>>(table, n >> logL, logL,
+                                                              pl->tw_img + dir * words + pl->tw_img_off[pi]);
+      WM_LAUNCH_CHECK("twiddle_image launch");
+    }
+  }
   WM_CUDA_TRY(cudaDeviceSynchronize());
   return WM_OK;
 }
@@ -722,6 +790,7 @@ int wm_ntt_plan_destroy(wm_ntt_plan *p) {
   if (p->tw_fwd) cudaFree(p->tw_fwd);
   if (p->tw_inv) cudaFree(p->tw_inv);
   if (p->tw_inv_scaled) cudaFree(p->tw_inv_scaled);
+  if (p->tw_img) cudaFree(p->tw_img);
   if (p->ws) cudaFree(p->ws);
   release_host_pipeline(p);
   delete p;
