@@ -70,6 +70,9 @@ struct PassDesc {
   int64_t total_lines;  // row passes: batch * lines_inner
   const uint32_t *mul_by;  // last pass: out[pos] = result[pos] * mul_by[pos] mod p (convolution)
   const uint32_t *tw_img;  // this pass's twiddle sub-table, pre-swizzled shared-memory image
+  // power-of-two strides as shifts (all index math in the element loops is
+  // shift/mask: no divisions, no 64-bit multiplies on the FMA pipe)
+  int logG, logn, log_inner, log_tiles_inner, logRT, logWK, logWO;
 };
 
 // ------------------------------------------------------------------ smem layout
@@ -89,7 +92,7 @@ struct Smem {
   WM_DEV static int swz(int e) {
     if constexpr (kSwz) {
       const int r = (e * C) >> 3;
-      return (r ^ (r >> 3) ^ (r >> 6) ^ (r >> 9) ^ (r >> 12)) & 7;
+      return (r ^ (r >> 3) ^ (r >> 6)) & 7;  // tiles are <= 512 rows of 128 B (plan_passes)
     } else {
       return 0;
     }
@@ -296,46 +299,50 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass
   uint32_t *tww = smem + tile_words<K>(logL, G);
   uint32_t *twp = tww + (size_t)(L / 2) * K;
   uint64_t *mbar = reinterpret_cast<uint64_t *>(tww + twimg_words<K>(logL));
-  const int64_t tiles_inner = d.lines_inner / G;
+  const int logG = d.logG;
   const int64_t tile = blockIdx.x;
-  const int64_t o = tile / tiles_inner;
-  const int64_t i0 = (tile - o * tiles_inner) * G;
-  const int64_t base = (int64_t)blockIdx.y * d.n;
+  const int64_t o = tile >> d.log_tiles_inner;
+  const int64_t i0 = (tile & (((int64_t)1 << d.log_tiles_inner) - 1)) << logG;
+  const int64_t base = (int64_t)blockIdx.y << d.logn;
+  const uint32_t *src = in + (base + o * d.RO + i0) * K;  // element (t, g) at src + ((t << logRT) + g) * K
+  uint32_t *dst = out + (base + o * d.WO + i0) * K;        // element (k, g) at dst + ((k << logWK) + g) * K
 
   twimg_issue(tww, d.tw_img, (uint32_t)(twimg_words<K>(logL) * 4), mbar);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
-    const int t = idx / G, g = idx - t * G;
-    const int64_t pos = base + o * d.RO + (int64_t)t * d.RT + i0 + g;
+    const int t = idx >> logG, g = idx & (G - 1);
     uint32_t v[K];
-    ldg_elem<K>(v, in + pos * K);
+    ldg_elem<K>(v, src + (((int64_t)t << d.logRT) + g) * K);
     const int tb = (int)(__brev((unsigned)t) >> (32 - logL));
     S::store(data, g * L + tb, v);
   }
   __syncthreads();
   twimg_wait(mbar);
   dft_smem<K>(data, tww, twp, logL, G, c);
-  const int64_t nmask = d.n - 1;
+  // inter-pass twiddle exponent, reduced mod n (n | 2^32, so 32-bit wraparound is exact)
+  const uint32_t nmask = (uint32_t)(d.n - 1);
+  const uint32_t oc1 = (uint32_t)(o * d.C1);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
-    const int k = idx / G, g = idx - k * G;
+    const int k = idx >> logG, g = idx & (G - 1);
     uint32_t v[K];
     S::load(v, data, g * L + k);
     if (d.C3) {
-      const int64_t e = ((((i0 + g) >> d.SH) * (o * d.C1 + (int64_t)k * d.C2)) * d.C3) & nmask;
+      const uint32_t e = ((uint32_t)((i0 + g) >> d.SH) * (oc1 + (uint32_t)k * (uint32_t)d.C2) *
+                          (uint32_t)d.C3) & nmask;
       uint32_t w[K], wp[K], r[K];
-      ldg_elem<K>(w, tw_out + e * (2 * K));
-      ldg_elem<K>(wp, tw_out + e * (2 * K) + K);
+      ldg_elem<K>(w, tw_out + (size_t)e * (2 * K));
+      ldg_elem<K>(wp, tw_out + (size_t)e * (2 * K) + K);
       mul_shoup_lazy<K>(r, v, w, wp, c.np);
       copy_n<K>(v, r);
     }
     if (d.canonical_out) canonical_6p<K>(v, c.p, c.p2, c.p4);
-    const int64_t pos = base + o * d.WO + (int64_t)k * d.WK + i0 + g;
+    const int64_t off = (((int64_t)k << d.logWK) + g) * K;
     if (d.mul_by) {
       uint32_t m[K], rr[K];
-      ldg_elem<K>(m, d.mul_by + pos * K);
+      ldg_elem<K>(m, d.mul_by + (dst - out) + off);
       mul_barrett<K>(rr, v, m, c.F);
       copy_n<K>(v, rr);
     }
-    stg_elem<K>(out + pos * K, v);
+    stg_elem<K>(dst + off, v);
   }
 }
 
@@ -352,17 +359,18 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass
   uint32_t *tww = smem + tile_words<K>(logL, G);
   uint32_t *twp = tww + (size_t)(L / 2) * K;
   uint64_t *mbar = reinterpret_cast<uint64_t *>(tww + twimg_words<K>(logL));
-  const int64_t lam0 = (int64_t)blockIdx.x * G;
+  const int64_t lam0 = (int64_t)blockIdx.x << d.logG;
+  const int64_t inner_mask = ((int64_t)1 << d.log_inner) - 1;
 
   twimg_issue(tww, d.tw_img, (uint32_t)(twimg_words<K>(logL) * 4), mbar);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
     const int g = idx >> logL, t = idx & (L - 1);
     const int64_t lam = lam0 + g;
     if (lam < d.total_lines) {
-      const int64_t b = lam / d.lines_inner, r = lam - b * d.lines_inner;
-      const int64_t pos = b * d.n + r * L + t;
+      // line lam = (b, r): b = lam >> log_inner, r = lam & inner_mask; lines of a
+      // transform are contiguous, so the line starts at element lam * L
       uint32_t v[K];
-      ldg_elem<K>(v, in + pos * K);
+      ldg_elem<K>(v, in + ((lam << logL) + t) * K);
       const int tb = (int)(__brev((unsigned)t) >> (32 - logL));
       S::store(data, g * L + tb, v);
     }
@@ -374,7 +382,7 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass
     const int g = idx >> logL, k = idx & (L - 1);
     const int64_t lam = lam0 + g;
     if (lam < d.total_lines) {
-      const int64_t b = lam / d.lines_inner, r = lam - b * d.lines_inner;
+      const int64_t b = lam >> d.log_inner, r = lam & inner_mask;
       uint32_t v[K];
       S::load(v, data, g * L + k);
       if (d.scale_out) {
@@ -383,7 +391,7 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass
         copy_n<K>(v, rr);
       }
       if (d.canonical_out) canonical_6p<K>(v, c.p, c.p2, c.p4);
-      const int64_t pos = b * d.n + r * d.WO + (int64_t)k * d.WK;
+      const int64_t pos = (b << d.logn) + (r << d.logWO) + ((int64_t)k << d.logWK);
       if (d.mul_by) {  // fused pointwise product (NTT-domain convolution)
         uint32_t m[K], rr[K];
         ldg_elem<K>(m, d.mul_by + pos * K);
@@ -490,6 +498,9 @@ static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
   return c;
 }
 
+// log2 of a power of two (every stride/count of a pass plan is one)
+static int ilog2_exact(int64_t v) { return 63 - __builtin_clzll((unsigned long long)v); }
+
 static size_t round4_h(size_t w) { return (w + 3) & ~(size_t)3; }
 static size_t twimg_bytes(int K, int logL) { return round4_h(((size_t)1 << logL) * K) * sizeof(uint32_t); }
 static size_t pass_smem(int K, const wm_pass_plan &ps) {
@@ -536,6 +547,13 @@ static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, u
     d.tw_stride = pl->n >> ps.logL;
     d.total_lines = batch * ps.lines_inner;
     d.mul_by = (pi + 1 == (int)pl->passes.size()) ? mul_by : nullptr;
+    d.logG = ilog2_exact(ps.G);
+    d.logn = pl->logn;
+    d.log_inner = ilog2_exact(ps.lines_inner);
+    d.log_tiles_inner = ps.column ? ilog2_exact(ps.lines_inner / ps.G) : 0;
+    d.logRT = ps.column ? ilog2_exact(ps.RT) : 0;
+    d.logWK = ilog2_exact(ps.WK);
+    d.logWO = ps.column ? 0 : (ps.lines_inner == 1 ? 0 : ilog2_exact(ps.WO));
     d.tw_img = pl->tw_img + (size_t)(inverse ? 1 : 0) * pl->tw_img_words_dir + pl->tw_img_off[pi];
     const size_t smem = pass_smem(K, ps);
     if (ps.column) {
@@ -668,6 +686,10 @@ static int plan_passes(wm_ntt_plan *pl) {
   pl->passes.back().canonical_out = true;
   for (const auto &ps : pl->passes) {
     if (pass_smem(K, ps) > 227 * 1024) return fail(WM_EUNSUPPORTED, "pass does not fit in shared memory");
+    // the shared-memory swizzle folds row indices below 512 (Smem<K>::swz)
+    const bool swizzled = (K % 4 == 0) && ((K / 4) & (K / 4 - 1)) == 0 && K / 4 <= 8;
+    if (swizzled && (size_t)ps.G * ((size_t)1 << ps.logL) * K * 4 > 512 * 128)
+      return fail(WM_EUNSUPPORTED, "pass tile above 64 KB");
   }
   return WM_OK;
 }
