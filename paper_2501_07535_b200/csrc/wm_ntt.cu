@@ -227,6 +227,14 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
   }
 }
 
+// Global loads kept in flight per thread while a pass stages its tile.
+template <int K>
+constexpr int kLoadU = K <= 8 ? 4 : (K <= 16 ? 2 : 1);
+
+// Column-pass epilogue: elements whose twiddle loads are issued together.
+template <int K>
+constexpr int kEpiU = K <= 8 ? 2 : 1;
+
 // Shared-memory map of a pass CTA (all offsets 16-byte aligned):
 //   [data tile: G*L elements][twiddle image: L/2 (w) + L/2 (w') elements][mbarrier]
 WM_DEV size_t round4(size_t words) { return (words + 3) & ~(size_t)3; }
@@ -308,12 +316,26 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass
   uint32_t *dst = out + (base + o * d.WO + i0) * K;        // element (k, g) at dst + ((k << logWK) + g) * K
 
   twimg_issue(tww, d.tw_img, (uint32_t)(twimg_words<K>(logL) * 4), mbar);
-  for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
-    const int t = idx >> logG, g = idx & (G - 1);
-    uint32_t v[K];
-    ldg_elem<K>(v, src + (((int64_t)t << d.logRT) + g) * K);
-    const int tb = (int)(__brev((unsigned)t) >> (32 - logL));
-    S::store(data, g * L + tb, v);
+  // U loads in flight per thread before their shared-memory stores
+  for (int i0x = threadIdx.x; i0x < G * L; i0x += kLoadU<K> * blockDim.x) {
+    uint32_t v[kLoadU<K>][K];
+#pragma unroll
+    for (int u = 0; u < kLoadU<K>; ++u) {
+      const int idx = i0x + u * blockDim.x;
+      if (idx < G * L) {
+        const int t = idx >> logG, g = idx & (G - 1);
+        ldg_elem<K>(v[u], src + (((int64_t)t << d.logRT) + g) * K);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kLoadU<K>; ++u) {
+      const int idx = i0x + u * blockDim.x;
+      if (idx < G * L) {
+        const int t = idx >> logG, g = idx & (G - 1);
+        const int tb = (int)(__brev((unsigned)t) >> (32 - logL));
+        S::store(data, g * L + tb, v[u]);
+      }
+    }
   }
   __syncthreads();
   twimg_wait(mbar);
@@ -321,28 +343,42 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass
   // inter-pass twiddle exponent, reduced mod n (n | 2^32, so 32-bit wraparound is exact)
   const uint32_t nmask = (uint32_t)(d.n - 1);
   const uint32_t oc1 = (uint32_t)(o * d.C1);
-  for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
-    const int k = idx >> logG, g = idx & (G - 1);
-    uint32_t v[K];
-    S::load(v, data, g * L + k);
-    if (d.C3) {
-      const uint32_t e = ((uint32_t)((i0 + g) >> d.SH) * (oc1 + (uint32_t)k * (uint32_t)d.C2) *
-                          (uint32_t)d.C3) & nmask;
-      uint32_t w[K], wp[K], r[K];
-      ldg_elem<K>(w, tw_out + (size_t)e * (2 * K));
-      ldg_elem<K>(wp, tw_out + (size_t)e * (2 * K) + K);
-      mul_shoup_lazy<K>(r, v, w, wp, c.np);
-      copy_n<K>(v, r);
+  constexpr int U = kEpiU<K>;
+  for (int i0x = threadIdx.x; i0x < G * L; i0x += U * blockDim.x) {
+    uint32_t w[U][K], wp[U][K];
+    if (d.C3) {  // inter-pass twiddles for all U elements in flight first
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = min(i0x + u * blockDim.x, G * L - 1);
+        const int k = idx >> logG, g = idx & (G - 1);
+        const uint32_t e = ((uint32_t)((i0 + g) >> d.SH) * (oc1 + (uint32_t)k * (uint32_t)d.C2) *
+                            (uint32_t)d.C3) & nmask;
+        ldg_elem<K>(w[u], tw_out + (size_t)e * (2 * K));
+        ldg_elem<K>(wp[u], tw_out + (size_t)e * (2 * K) + K);
+      }
     }
-    if (d.canonical_out) canonical_6p<K>(v, c.p, c.p2, c.p4);
-    const int64_t off = (((int64_t)k << d.logWK) + g) * K;
-    if (d.mul_by) {
-      uint32_t m[K], rr[K];
-      ldg_elem<K>(m, d.mul_by + (dst - out) + off);
-      mul_barrett<K>(rr, v, m, c.F);
-      copy_n<K>(v, rr);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = i0x + u * blockDim.x;
+      if (U > 1 && idx >= G * L) break;
+      const int k = idx >> logG, g = idx & (G - 1);
+      uint32_t v[K];
+      S::load(v, data, g * L + k);
+      if (d.C3) {
+        uint32_t r[K];
+        mul_shoup_lazy<K>(r, v, w[u], wp[u], c.np);
+        copy_n<K>(v, r);
+      }
+      if (d.canonical_out) canonical_6p<K>(v, c.p, c.p2, c.p4);
+      const int64_t off = (((int64_t)k << d.logWK) + g) * K;
+      if (d.mul_by) {
+        uint32_t m[K], rr[K];
+        ldg_elem<K>(m, d.mul_by + (dst - out) + off);
+        mul_barrett<K>(rr, v, m, c.F);
+        copy_n<K>(v, rr);
+      }
+      stg_elem<K>(dst + off, v);
     }
-    stg_elem<K>(dst + off, v);
   }
 }
 
@@ -363,16 +399,24 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass
   const int64_t inner_mask = ((int64_t)1 << d.log_inner) - 1;
 
   twimg_issue(tww, d.tw_img, (uint32_t)(twimg_words<K>(logL) * 4), mbar);
-  for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
-    const int g = idx >> logL, t = idx & (L - 1);
-    const int64_t lam = lam0 + g;
-    if (lam < d.total_lines) {
-      // line lam = (b, r): b = lam >> log_inner, r = lam & inner_mask; lines of a
-      // transform are contiguous, so the line starts at element lam * L
-      uint32_t v[K];
-      ldg_elem<K>(v, in + ((lam << logL) + t) * K);
-      const int tb = (int)(__brev((unsigned)t) >> (32 - logL));
-      S::store(data, g * L + tb, v);
+  // line lam = (b, r): b = lam >> log_inner, r = lam & inner_mask; lines of a
+  // transform are contiguous, so the line starts at element lam * L
+  for (int i0x = threadIdx.x; i0x < G * L; i0x += kLoadU<K> * blockDim.x) {
+    uint32_t v[kLoadU<K>][K];
+#pragma unroll
+    for (int u = 0; u < kLoadU<K>; ++u) {
+      const int idx = i0x + u * blockDim.x;
+      const int64_t lam = lam0 + (idx >> logL);
+      if (idx < G * L && lam < d.total_lines) ldg_elem<K>(v[u], in + ((lam << logL) + (idx & (L - 1))) * K);
+    }
+#pragma unroll
+    for (int u = 0; u < kLoadU<K>; ++u) {
+      const int idx = i0x + u * blockDim.x;
+      const int g = idx >> logL, t = idx & (L - 1);
+      if (idx < G * L && lam0 + g < d.total_lines) {
+        const int tb = (int)(__brev((unsigned)t) >> (32 - logL));
+        S::store(data, g * L + tb, v[u]);
+      }
     }
   }
   __syncthreads();
