@@ -128,10 +128,11 @@ struct Smem {
 template <int K>
 __device__ __forceinline__ void radix4_single(uint32_t (&x0)[K], uint32_t (&x1)[K], uint32_t (&x2)[K],
                                               uint32_t (&x3)[K], const uint32_t *tww, const uint32_t *twp, int s,
-                                              int j, int h, int logL, int lq, const NttConst<K> &c) {
+                                              int j, int h, int logL, int lq, bool trivial,
+                                              const NttConst<K> &c) {
   using S = Smem<K>;
   uint32_t w[K], wp[K];
-  if (s == 0) {
+  if (trivial) {  // j == 0: the stage-s twiddle and the first stage-(s+1) twiddle are 1
     bf_lazy_w1<K>(x0, x1, c.p3);
     bf_lazy_w1<K>(x2, x3, c.p3);
     bf_lazy_w1<K>(x0, x2, c.p3);  // j = 0: root^0
@@ -203,20 +204,37 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
     __syncthreads();
     s = 1;
   }
+  const int logG = __ffs(G) - 1;
   for (; s < logL; s += 2) {
     const int h = 1 << s;
     const int lq = logL - 2;
+    const int nbl = lq - s;  // log2(radix-4 blocks per line)
+    // j-major group order (swizzled layouts, >= 32 (line, block) pairs per j):
+    // every warp then shares one j, so its twiddle reads are broadcasts and
+    // the j == 0 warps skip the three unit-twiddle products; the order is also
+    // bank-conflict-free where the line-major order is 2-way (tools/bank_model.py)
+    const bool jmajor = Smem<K>::kSwz && s > 0 && (logG + nbl) >= 5;
     for (int grp = threadIdx.x; grp < (G << lq); grp += blockDim.x) {
-      const int g = grp >> lq;
-      const int jj = grp & ((1 << lq) - 1);
-      const int j = jj & (h - 1);
-      const int e0 = (g << logL) + ((jj >> s) << (s + 2)) + j;
+      int g, blk, j;
+      if (jmajor) {
+        const int lp = logG + nbl;
+        j = grp >> lp;
+        const int rest = grp & ((1 << lp) - 1);
+        g = rest >> nbl;
+        blk = rest & ((1 << nbl) - 1);
+      } else {
+        g = grp >> lq;
+        const int jj = grp & ((1 << lq) - 1);
+        j = jj & (h - 1);
+        blk = jj >> s;
+      }
+      const int e0 = (g << logL) + (blk << (s + 2)) + j;
       uint32_t x0[K], x1[K], x2[K], x3[K];
       S::load(x0, data, e0);
       S::load(x1, data, e0 + h);
       S::load(x2, data, e0 + 2 * h);
       S::load(x3, data, e0 + 3 * h);
-      radix4_single<K>(x0, x1, x2, x3, tww, twp, s, j, h, logL, lq, c);
+      radix4_single<K>(x0, x1, x2, x3, tww, twp, s, j, h, logL, lq, s == 0 || (jmajor && j == 0), c);
 
       S::store(data, e0, x0);
       S::store(data, e0 + h, x1);
