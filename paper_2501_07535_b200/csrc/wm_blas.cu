@@ -122,20 +122,6 @@ Big big_pow2_div(int e, const Big &d, int limbs) {
 }
 
 // ------------------------------------------------------------------ field
-template <int K>
-FieldConst<K> field_const(const wm_field *f) {
-  FieldConst<K> c;
-  for (int j = 0; j < K; ++j) {
-    c.q[j] = f->q[j];
-    c.qn[j] = f->qn[j];
-    c.qn2[j] = f->qn2[j];
-    c.nqn[j] = f->nqn[j];
-    c.mu8[j] = f->mu8[j];
-  }
-  c.s = (uint32_t)f->s;
-  return c;
-}
-
 // ------------------------------------------------------------------ kernels
 enum BlasOp { OP_VADD = 0, OP_VSUB = 1, OP_VMUL = 2, OP_AXPY = 3 };
 

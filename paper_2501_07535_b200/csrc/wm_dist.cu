@@ -148,19 +148,6 @@ __global__ void twiddle_2d_kernel(uint32_t *table, int64_t n, int64_t row0, int6
   }
 }
 
-template <int K>
-static FieldConst<K> fconst(const wm_field *f) {
-  FieldConst<K> c;
-  for (int j = 0; j < K; ++j) {
-    c.q[j] = f->q[j];
-    c.qn[j] = f->qn[j];
-    c.qn2[j] = f->qn2[j];
-    c.nqn[j] = f->nqn[j];
-    c.mu8[j] = f->mu8[j];
-  }
-  c.s = (uint32_t)f->s;
-  return c;
-}
 
 template <int K>
 static int launch_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out,
@@ -173,7 +160,7 @@ static int launch_scale_transpose(const wm_field *f, const uint32_t *in, const u
     attr = true;
   }
   dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)((rows + TT - 1) / TT));
-  scale_transpose_kernel<K><<<grid, 256, smem, st>>>(in, table, out, rows, cols, fconst<K>(f));
+  scale_transpose_kernel<K><<<grid, 256, smem, st>>>(in, table, out, rows, cols, field_const<K>(f));
   WM_LAUNCH_CHECK("scale_transpose launch");
   return WM_OK;
 }
@@ -186,7 +173,7 @@ static int launch_twiddle_2d(const wm_field *f, int64_t n, const uint32_t *root,
   const int64_t chunk = 64;
   const int64_t threads = rows * ((cols + chunk - 1) / chunk);
   const int grid = (int)((threads + 127) / 128);
-  twiddle_2d_kernel<K><<<grid, 128, 0, st>>>(table, n, row0, rows, cols, chunk, fconst<K>(f), rt);
+  twiddle_2d_kernel<K><<<grid, 128, 0, st>>>(table, n, row0, rows, cols, chunk, field_const<K>(f), rt);
   WM_LAUNCH_CHECK("twiddle_2d launch");
   return WM_OK;
 }

@@ -113,6 +113,21 @@ struct wm_ntt_plan {
 };
 
 namespace wm {
+// Device constants of a field (the one place they are packed for kernels).
+template <int K>
+inline FieldConst<K> field_const(const wm_field *f) {
+  FieldConst<K> c;
+  for (int j = 0; j < K; ++j) {
+    c.q[j] = f->q[j];
+    c.qn[j] = f->qn[j];
+    c.qn2[j] = f->qn2[j];
+    c.nqn[j] = f->nqn[j];
+    c.mu8[j] = f->mu8[j];
+  }
+  c.s = (uint32_t)f->s;
+  return c;
+}
+
 int ntt_run_internal(const wm_ntt_plan *p, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
                      void *workspace, cudaStream_t st, const uint32_t *mul_by = nullptr);
 int release_host_pipeline(wm_ntt_plan *p);

@@ -162,9 +162,9 @@ WM_DEV void mul_full_ptx(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uin
 // columns >= C0 = K-2 only (partial products a_j*b_i with i+j < C0 and their
 // carries are dropped).  The neglected sum is < C0 * 2^(32(C0+1)) < 2^(32K-27),
 // so the result is the exact high half or one less.  K^2 - (K-2)(K-1)/2 products.
-template <int K>
+template <int K, int D = 2>
 WM_DEV void mul_hi_trunc_ptx(uint32_t (&h)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
-  constexpr int C0 = (K > 2) ? K - 2 : 0;
+  constexpr int C0 = (K > D) ? K - D : 0;
   constexpr int W = 2 * K - C0;  // columns C0 .. 2K-1, acc[c - C0]
   uint32_t acc[W + 1];
 #pragma unroll
@@ -253,9 +253,9 @@ WM_DEV void mul_full_u64(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uin
   }
 }
 
-template <int K>
+template <int K, int D = 2>
 WM_DEV void mul_hi_trunc_u64(uint32_t (&h)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
-  constexpr int C0 = (K > 2) ? K - 2 : 0;
+  constexpr int C0 = (K > D) ? K - D : 0;
   constexpr int W = 2 * K - C0;
   uint32_t acc[W];
 #pragma unroll
@@ -302,9 +302,11 @@ template <int K, int ST = kPtx>
 WM_DEV void mul_full(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
   if constexpr (ST == kPtx) mul_full_ptx<K>(t, a, b); else mul_full_u64<K>(t, a, b);
 }
-template <int K, int ST = kPtx>
+// D = 2: columns >= K-2 (result exact or one less); D = 1: columns >= K-1
+// (K(K+1)/2 products, result within K of the exact high half).
+template <int K, int ST = kPtx, int D = 2>
 WM_DEV void mul_hi_trunc(uint32_t (&h)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
-  if constexpr (ST == kPtx) mul_hi_trunc_ptx<K>(h, a, b); else mul_hi_trunc_u64<K>(h, a, b);
+  if constexpr (ST == kPtx) mul_hi_trunc_ptx<K, D>(h, a, b); else mul_hi_trunc_u64<K, D>(h, a, b);
 }
 template <int K, int ST = kPtx>
 WM_DEV void mul_lo_acc(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {

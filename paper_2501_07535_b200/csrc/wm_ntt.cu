@@ -514,24 +514,11 @@ __global__ void twiddle_extract_kernel(const uint32_t *table, int64_t count, uin
 }
 
 // ------------------------------------------------------------------ host side
-template <int K>
-static FieldConst<K> field_const_local(const wm_field *f) {
-  FieldConst<K> c;
-  for (int j = 0; j < K; ++j) {
-    c.q[j] = f->q[j];
-    c.qn[j] = f->qn[j];
-    c.qn2[j] = f->qn2[j];
-    c.nqn[j] = f->nqn[j];
-    c.mu8[j] = f->mu8[j];
-  }
-  c.s = (uint32_t)f->s;
-  return c;
-}
 
 template <int K>
 static int gen_table(const wm_field *f, uint32_t *table, int64_t count, const Big &base, const Big &scale) {
   TwGenArgs<K> a;
-  a.F = field_const_local<K>(f);
+  a.F = field_const<K>(f);
   for (int j = 0; j < K; ++j) {
     a.base[j] = base[j];
     a.scale[j] = scale[j];
@@ -547,7 +534,7 @@ static int gen_table(const wm_field *f, uint32_t *table, int64_t count, const Bi
 template <int K>
 static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
   NttConst<K> c;
-  c.F = field_const_local<K>(pl->field);
+  c.F = field_const<K>(pl->field);
   for (int j = 0; j < K; ++j) {
     c.p[j] = pl->field->q[j];
     c.p2[j] = pl->p2[j];

@@ -34,6 +34,9 @@ a = torch.randint(0, 1 << 27, (n, 8), dtype=torch.int32, device="cuda"); b = a.f
 o = torch.empty_like(a)
 f = dev.Field(256, find_ntt_params(256, 1).p)
 res["vmul256_GBps"] = round(96 * n / t(lambda: f.vmul(a, b, out=o)) / 1e6, 1)
+fk = dev.Field(256, find_ntt_params(256, 1).p, "karatsuba")
+res["vmul256_kara_GBps"] = round(96 * n / t(lambda: fk.vmul(a, b, out=o)) / 1e6, 1)
+ref = f.vmul(a, b, out=torch.empty_like(a)); assert torch.equal(fk.vmul(a, b, out=o), ref)
 print(json.dumps(res))
 ''' % str(ROOT)
 for lib in sys.argv[1:]:
