@@ -55,9 +55,16 @@ def dist_setup(gpus: int):
             raise SystemExit("--gpus N>1 must be launched with torchrun (one process per GPU)")
     pg = None
     if world > 1:
+        import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl" if _cuda_ok() else "gloo")
+        if _cuda_ok():
+            # bind the rank to its GPU before NCCL initialises (barriers and
+            # collectives then use the right device)
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
         pg = dist
     return rank, world, local, pg
 
@@ -276,8 +283,20 @@ def run_e2e(args, torch, dev, plan, field, ws, pg, world):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = max_over_ranks(pg, e0.elapsed_time(e1))
+    # the same pipeline with the transforms left out: the PCIe floor of the call
+    plan.host_transform(host_in, host_out, mode="copy", word_bits=64, ref_words=WORDS64, chunk=args.e2e_chunk)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        plan.host_transform(host_in, host_out, mode="copy", word_bits=64, ref_words=WORDS64,
+                            chunk=args.e2e_chunk)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    floor_ms = max_over_ranks(pg, e0.elapsed_time(e1))
     nbytes = host_in.numel() * host_in.element_size()
     return {"value": ms * 1e3 / (world * args.steps * 2 * BATCH), "unit": UNIT,
+            "copy_floor": floor_ms * 1e3 / (world * args.steps * 2 * BATCH),
+            "copy_floor_basis": "same wm_ntt_host pipeline, mode=COPY (H2D, layout convert, D2H; no transform)",
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
             "path": "NttPlan.host_transform -> C ABI wm_ntt_host(mode=FWD_INV): pinned host buffers, "
                     "reference layout, chunked H2D/compute/D2H pipeline",

@@ -160,11 +160,13 @@ int wm_ntt_twiddles(const wm_ntt_plan *p, int inverse, int64_t count, uint32_t *
  * D2H copy — so PCIe traffic in both directions overlaps the kernels.  Host
  * buffers should be pinned (cudaHostAlloc / cudaHostRegister) for overlap.
  * mode: WM_NTT_FWD, WM_NTT_INV, or WM_NTT_FWD_INV (forward then inverse, the
- * benchmark's round trip).  Ordered after prior work on `stream`; `stream`
+ * benchmark's round trip); WM_NTT_COPY runs the same pipeline with the layout
+ * conversions but no transform (the PCIe floor of the path, for measurement).  Ordered after prior work on `stream`; `stream`
  * waits for the whole pipeline, so event timing on it brackets everything. */
 #define WM_NTT_FWD 0
 #define WM_NTT_INV 1
 #define WM_NTT_FWD_INV 2
+#define WM_NTT_COPY 3
 int wm_ntt_host(const wm_ntt_plan *p, int mode, int word_bits, int ref_words, const void *host_in,
                 void *host_out, int64_t batch, int64_t chunk, void *stream);
 

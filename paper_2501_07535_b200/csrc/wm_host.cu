@@ -4,13 +4,16 @@
 // against the kernels ("the host boundary's
 // throughput").
 //
-// Three plan-owned streams form a pipeline over chunks of `chunk` transforms
-// with kSlots staging slots in device memory:
-//   h2d stream:     wait slot free -> memcpy host_in chunk -> record ev_in
-//   compute stream: wait ev_in -> ref->limbs, NTT[/INTT], limbs->ref -> ev_comp
-//   d2h stream:     wait ev_comp -> memcpy to host_out -> record ev_out (slot free)
-// PCIe is full duplex, so the H2D of chunk c+1, the kernels of chunk c and the
-// D2H of chunk c-1 all run at once.
+// Plan-owned streams form a pipeline over chunks of `chunk` transforms with
+// kSlots staging slots in device memory:
+//   h2d stream:      wait slot free -> memcpy host_in chunk -> record ev_in
+//   compute streams: wait ev_in -> ref->limbs, NTT[/INTT], limbs->ref -> ev_comp
+//   d2h stream:      wait ev_comp -> memcpy to host_out -> record ev_out (slot free)
+// PCIe is full duplex, so H2D and D2H of different chunks run at once.  A
+// small chunk's kernels fill only part of the GPU (a 2^16-point, 256-bit
+// chunk of 2 transforms is 64 CTAs per pass), so chunks round-robin over
+// kComp compute streams and the kernels of consecutive chunks run
+// concurrently; the copies, not the kernels, then bound the pipeline.
 #include <algorithm>
 
 #include "wm_internal.cuh"
@@ -19,7 +22,8 @@ namespace wm {
 
 static int ensure_host_pipeline(wm_ntt_plan *p, int64_t slot_bytes) {
   if (!p->host_ready) {
-    for (int i = 0; i < 3; ++i) WM_CUDA_TRY(cudaStreamCreateWithFlags(&p->hs[i], cudaStreamNonBlocking));
+    for (int i = 0; i < wm_ntt_plan::kStreams; ++i)
+      WM_CUDA_TRY(cudaStreamCreateWithFlags(&p->hs[i], cudaStreamNonBlocking));
     for (int s = 0; s < wm_ntt_plan::kSlots; ++s) {
       WM_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_in[s], cudaEventDisableTiming));
       WM_CUDA_TRY(cudaEventCreateWithFlags(&p->ev_comp[s], cudaEventDisableTiming));
@@ -30,7 +34,7 @@ static int ensure_host_pipeline(wm_ntt_plan *p, int64_t slot_bytes) {
     p->host_ready = true;
   }
   if (p->slot_bytes < slot_bytes) {
-    for (int i = 0; i < 3; ++i) WM_CUDA_TRY(cudaStreamSynchronize(p->hs[i]));
+    for (int i = 0; i < wm_ntt_plan::kStreams; ++i) WM_CUDA_TRY(cudaStreamSynchronize(p->hs[i]));
     for (int s = 0; s < wm_ntt_plan::kSlots; ++s) {
       if (p->slot_mem[s]) WM_CUDA_TRY(cudaFree(p->slot_mem[s]));
       p->slot_mem[s] = nullptr;
@@ -44,7 +48,7 @@ static int ensure_host_pipeline(wm_ntt_plan *p, int64_t slot_bytes) {
 
 int release_host_pipeline(wm_ntt_plan *p) {
   if (!p->host_ready) return WM_OK;
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < wm_ntt_plan::kStreams; ++i) {
     cudaStreamSynchronize(p->hs[i]);
     cudaStreamDestroy(p->hs[i]);
   }
@@ -69,7 +73,7 @@ using namespace wm;
 extern "C" int wm_ntt_host(const wm_ntt_plan *pc, int mode, int word_bits, int ref_words, const void *host_in,
                            void *host_out, int64_t batch, int64_t chunk, void *stream) {
   if (!pc) return fail(WM_EINVAL, "null plan");
-  if (mode < WM_NTT_FWD || mode > WM_NTT_FWD_INV) return fail(WM_EINVAL, "bad mode");
+  if (mode < WM_NTT_FWD || mode > WM_NTT_COPY) return fail(WM_EINVAL, "bad mode");
   if (word_bits != 32 && word_bits != 64) return fail(WM_EINVAL, "word_bits must be 32 or 64");
   if ((int64_t)ref_words * word_bits < pc->field->bits) return fail(WM_EINVAL, "reference words too narrow");
   if (batch < 0 || chunk < 0) return fail(WM_EINVAL, "negative batch/chunk");
@@ -78,7 +82,7 @@ extern "C" int wm_ntt_host(const wm_ntt_plan *pc, int mode, int word_bits, int r
   wm_ntt_plan *p = const_cast<wm_ntt_plan *>(pc);
   const int64_t n = p->n;
   const int K = p->K;
-  if (chunk == 0) chunk = std::max<int64_t>(1, (int64_t)(8 << 20) / (n * K * 4));  // ~8 MiB of limbs (tools/e2e_probe.py)
+  if (chunk == 0) chunk = std::max<int64_t>(1, (int64_t)(4 << 20) / (n * K * 4));  // ~4 MiB of limbs (tools/e2e_sweep.sh)
   chunk = std::min(chunk, batch);
   const size_t ref_bytes_per_t = (size_t)n * ref_words * (word_bits / 8);
   const size_t limb_bytes_per_t = (size_t)n * K * 4;
@@ -91,15 +95,14 @@ extern "C" int wm_ntt_host(const wm_ntt_plan *pc, int mode, int word_bits, int r
   int rc = ensure_host_pipeline(p, (int64_t)slot);
   if (rc) return rc;
   cudaStream_t user = (cudaStream_t)stream;
-  cudaStream_t h2d = p->hs[0], comp = p->hs[1], d2h = p->hs[2];
+  cudaStream_t h2d = p->hs[0], d2h = p->hs[1];
   WM_CUDA_TRY(cudaEventRecord(p->ev_entry, user));
-  WM_CUDA_TRY(cudaStreamWaitEvent(h2d, p->ev_entry, 0));
-  WM_CUDA_TRY(cudaStreamWaitEvent(comp, p->ev_entry, 0));
-  WM_CUDA_TRY(cudaStreamWaitEvent(d2h, p->ev_entry, 0));
+  for (int i = 0; i < wm_ntt_plan::kStreams; ++i) WM_CUDA_TRY(cudaStreamWaitEvent(p->hs[i], p->ev_entry, 0));
 
   const int64_t nchunks = (batch + chunk - 1) / chunk;
   for (int64_t c = 0; c < nchunks; ++c) {
     const int s = (int)(c % wm_ntt_plan::kSlots);
+    cudaStream_t comp = p->hs[2 + c % wm_ntt_plan::kComp];
     const int64_t t0 = c * chunk;
     const int64_t nt = std::min(chunk, batch - t0);
     char *base = static_cast<char *>(p->slot_mem[s]);
@@ -140,7 +143,7 @@ extern "C" int wm_ntt_host(const wm_ntt_plan *pc, int mode, int word_bits, int r
   WM_CUDA_TRY(cudaEventRecord(p->ev_done, d2h));
   WM_CUDA_TRY(cudaStreamWaitEvent(user, p->ev_done, 0));
   // keep the other internal streams ordered behind the finished pipeline
-  WM_CUDA_TRY(cudaStreamWaitEvent(h2d, p->ev_done, 0));
-  WM_CUDA_TRY(cudaStreamWaitEvent(comp, p->ev_done, 0));
+  for (int i = 0; i < wm_ntt_plan::kStreams; ++i)
+    if (p->hs[i] != d2h) WM_CUDA_TRY(cudaStreamWaitEvent(p->hs[i], p->ev_done, 0));
   return WM_OK;
 }

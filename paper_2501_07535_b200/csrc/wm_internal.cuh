@@ -105,10 +105,14 @@ struct wm_ntt_plan {
   // host pipeline (wm_ntt_host): internal streams, events and staging slots
   std::mutex host_mu;
   bool host_ready = false;
-  cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // h2d, compute, d2h
-  static constexpr int kSlots = 3;
+  // h2d, d2h, then kComp compute streams: chunks round-robin over the compute
+  // streams so the kernels of consecutive (small) chunks share the GPU
+  static constexpr int kComp = 4;
+  static constexpr int kStreams = 2 + kComp;
+  cudaStream_t hs[kStreams] = {};
+  static constexpr int kSlots = 8;
   cudaEvent_t ev_in[kSlots], ev_comp[kSlots], ev_out[kSlots], ev_entry = nullptr, ev_done = nullptr;
-  void *slot_mem[kSlots] = {nullptr, nullptr, nullptr};
+  void *slot_mem[kSlots] = {};
   int64_t slot_bytes = 0;
 };
 

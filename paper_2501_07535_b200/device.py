@@ -291,10 +291,11 @@ class NttPlan:
         """End-to-end transform of HOST tensors in the reference layout (AoS,
         MSW-first words, kernels.to_words) through the pipelined C ABI call
         ``wm_ntt_host``: chunked H2D / kernels / D2H overlap.  mode is
-        "forward", "inverse" or "forward_inverse".  Pinned host tensors give
+        "forward", "inverse" or "forward_inverse" ("copy": the same pipeline
+        without the transform, i.e. the PCIe floor of the call).  Pinned host tensors give
         full PCIe overlap."""
         codes = {"forward": _lib.WM_NTT_FWD, "inverse": _lib.WM_NTT_INV,
-                 "forward_inverse": _lib.WM_NTT_FWD_INV}
+                 "forward_inverse": _lib.WM_NTT_FWD_INV, "copy": _lib.WM_NTT_COPY}
         if mode not in codes:
             raise ValueError(f"bad mode {mode!r}")
         if ref_words is None:
