@@ -184,7 +184,7 @@ def test_in_place_batch_and_workspace(cuda):
         plan.forward(dev.to_device(xl[: n - 1]))
 
 
-@pytest.mark.parametrize("mode", ["forward", "inverse", "forward_inverse"])
+@pytest.mark.parametrize("mode", ["forward", "inverse", "forward_inverse", "copy"])
 def test_host_pipeline_reference_layout(cuda, mode):
     """wm_ntt_host: pinned host buffers in the reference AoS MSW-first layout
     through the chunked H2D / kernels / D2H pipeline equal the device path."""
@@ -209,6 +209,6 @@ def test_host_pipeline_reference_layout(cuda, mode):
             want = plan.forward(xd)
         elif mode == "inverse":
             want = plan.inverse(xd)
-        else:
+        else:  # forward_inverse round trip, or the copy-only pipeline
             want = xd
         assert got == dev.limbs_to_ints(dev.to_host(want)), chunk
