@@ -181,6 +181,16 @@ int wm_transpose(int words, const uint32_t *in, uint32_t *out, int64_t rows, int
                  int64_t batch, void *stream);
 int wm_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out,
                        int64_t rows, int64_t cols, void *stream);
+
+/* wm_scale_transpose with the all-to-all fused in: output row c is stored into
+ * dst_ptrs[c / (cols/P)] at [src_rank][c mod (cols/P)][0..rows) of that rank's
+ * receive buffer ([P][cols/P][rows] elements).  dst_ptrs (host array of P
+ * device addresses, P <= 16) are peer-mapped buffers (symmetric memory over
+ * NVLink) or local buffers.  Replaces the exchange step the reference does not
+ * have. */
+int wm_scale_transpose_scatter(const wm_field *f, const uint32_t *in, const uint32_t *table,
+                               const uint64_t *dst_ptrs, int P, int src_rank, int64_t rows, int64_t cols,
+                               void *stream);
 int wm_twiddle_table_2d(const wm_field *f, int64_t n, const uint32_t *root_host, int64_t row0,
                         int64_t rows, int64_t cols, uint32_t *table, void *stream);
 

@@ -4,7 +4,9 @@
 // j2 = 0..N2-1), the forward transform is
 //   (a) N2-point row NTTs                  (wm_ntt_forward, batch N1/P)
 //   (b) Z[j1][k2] *= root^(j1 k2), transpose to [k2][j1]   (wm_scale_transpose)
-//   (c) all-to-all of the P column blocks  (NCCL, torch.distributed)
+//   (c) all-to-all of the P column blocks  (NCCL, torch.distributed), or fused
+//       into (b): wm_scale_transpose_scatter stores each block straight into
+//       its destination rank's receive buffer over NVLink (symmetric memory)
 //   (d) [P][N2/P][N1/P] -> [N2/P][P][N1/P] (wm_transpose on N1/P-element blocks)
 //   (e) N1-point row NTTs                  (wm_ntt_forward, batch N2/P)
 // leaving rank r with rows k2 in its block, row k2 = y[k2 + N2 k1].  The
@@ -69,12 +71,29 @@ __global__ void __launch_bounds__(256) transpose_wide_kernel(const uint32_t *in,
   }
 }
 
+// Destinations of the fused exchange: output row c (of `cols`) belongs to
+// rank c / cpr and lands in that rank's receive buffer, laid out
+// [P source ranks][cpr rows][rows elements], at source slot `src`.  The
+// pointers are peer-mapped (symmetric memory over NVLink) on a multi-GPU box,
+// or plain local buffers for virtual ranks on one GPU.
+constexpr int kMaxPeers = 16;
+struct ScatterDst {
+  uint64_t ptr[kMaxPeers];
+  int P;        // 0: no scatter, write `out`
+  int src;      // this rank
+  int64_t cpr;  // output rows per destination rank (cols / P)
+};
+
 // out[c][r] = in[r][c] * table[r][c] (mod p), K-limb elements, canonical out.
-// table entries are (w, w') Shoup pairs (2K words).
+// table entries are (w, w') Shoup pairs (2K words).  With a ScatterDst the
+// transposed tile rows are stored straight into the destination ranks'
+// receive buffers (the four-step all-to-all fused into the producing kernel:
+// each 32-element row segment is one coalesced remote store burst).
 template <int K>
 __global__ void __launch_bounds__(256) scale_transpose_kernel(const uint32_t *in, const uint32_t *table,
                                                               uint32_t *out, int64_t rows, int64_t cols,
-                                                              const __grid_constant__ FieldConst<K> F) {
+                                                              const __grid_constant__ FieldConst<K> F,
+                                                              const __grid_constant__ ScatterDst D) {
   extern __shared__ uint32_t tile[];  // TT * (TT*K + 1)
   const int64_t r0 = (int64_t)blockIdx.y * TT, c0 = (int64_t)blockIdx.x * TT;
   const int stride = TT * K + 1;
@@ -105,7 +124,16 @@ __global__ void __launch_bounds__(256) scale_transpose_kernel(const uint32_t *in
     const int cc = idx / (TT * K), w = idx - cc * (TT * K);
     const int rr = w / K, ww = w - rr * K;
     const int64_t c = c0 + cc, r = r0 + rr;
-    if (r < rows && c < cols) out[(c * rows + r0) * K + w] = tile[rr * stride + cc * K + ww];
+    if (r < rows && c < cols) {
+      uint32_t *row_base;
+      if (D.P > 0) {
+        const int64_t d = c / D.cpr, cl = c - d * D.cpr;
+        row_base = reinterpret_cast<uint32_t *>(D.ptr[d]) + ((int64_t)D.src * D.cpr + cl) * rows * K;
+      } else {
+        row_base = out + c * rows * K;
+      }
+      row_base[r0 * K + w] = tile[rr * stride + cc * K + ww];
+    }
   }
 }
 
@@ -151,7 +179,7 @@ __global__ void twiddle_2d_kernel(uint32_t *table, int64_t n, int64_t row0, int6
 
 template <int K>
 static int launch_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out,
-                                  int64_t rows, int64_t cols, cudaStream_t st) {
+                                  int64_t rows, int64_t cols, cudaStream_t st, const ScatterDst &D) {
   const size_t smem = (size_t)TT * (TT * K + 1) * 4;
   static bool attr = false;
   if (!attr) {
@@ -160,7 +188,7 @@ static int launch_scale_transpose(const wm_field *f, const uint32_t *in, const u
     attr = true;
   }
   dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)((rows + TT - 1) / TT));
-  scale_transpose_kernel<K><<<grid, 256, smem, st>>>(in, table, out, rows, cols, field_const<K>(f));
+  scale_transpose_kernel<K><<<grid, 256, smem, st>>>(in, table, out, rows, cols, field_const<K>(f), D);
   WM_LAUNCH_CHECK("scale_transpose launch");
   return WM_OK;
 }
@@ -216,10 +244,42 @@ int wm_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *ta
   if (rows == 0 || cols == 0) return WM_OK;
   if (!in || !table || !out || in == out) return fail(WM_EINVAL, "bad pointers (in/out must differ)");
   cudaStream_t st = (cudaStream_t)stream;
+  ScatterDst D{};
   switch (f->K) {
 #define WM_CASE(k) \
   case k:          \
-    return launch_scale_transpose<k>(f, in, table, out, rows, cols, st);
+    return launch_scale_transpose<k>(f, in, table, out, rows, cols, st, D);
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      return fail(WM_EUNSUPPORTED, "limb count not built in");
+  }
+}
+
+int wm_scale_transpose_scatter(const wm_field *f, const uint32_t *in, const uint32_t *table,
+                               const uint64_t *dst_ptrs, int P, int src_rank, int64_t rows, int64_t cols,
+                               void *stream) {
+  if (!f) return fail(WM_EINVAL, "null field");
+  if (rows < 0 || cols < 0) return fail(WM_EINVAL, "bad shape");
+  if (P < 1 || P > kMaxPeers) return fail(WM_EUNSUPPORTED, "peer count outside 1..16");
+  if (src_rank < 0 || src_rank >= P) return fail(WM_EINVAL, "source rank outside 0..P-1");
+  if (cols % P) return fail(WM_EINVAL, "P must divide cols");
+  if (rows == 0 || cols == 0) return WM_OK;
+  if (!in || !table || !dst_ptrs) return fail(WM_EINVAL, "null pointer");
+  ScatterDst D{};
+  for (int d = 0; d < P; ++d) {
+    if (!dst_ptrs[d]) return fail(WM_EINVAL, "null destination pointer");
+    if (dst_ptrs[d] == (uint64_t)(uintptr_t)in) return fail(WM_EINVAL, "destination aliases the input");
+    D.ptr[d] = dst_ptrs[d];
+  }
+  D.P = P;
+  D.src = src_rank;
+  D.cpr = cols / P;
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (f->K) {
+#define WM_CASE(k) \
+  case k:          \
+    return launch_scale_transpose<k>(f, in, table, nullptr, rows, cols, st, D);
     WM_NTT_KS(WM_CASE)
 #undef WM_CASE
     default:

@@ -65,8 +65,7 @@ struct PassDesc {
   int SH;
   int64_t C1, C2, C3;
   int scale_out;      // multiply outputs by n^-1 (one-pass inverse)
-  int canonical_out;  // last pass: reduce [0, 4p) -> [0, p)
-  int64_t tw_stride;  // n / L
+  int canonical_out;  // last pass: reduce [0, 6p) -> [0, p)
   int64_t total_lines;  // row passes: batch * lines_inner
   const uint32_t *mul_by;  // last pass: out[pos] = result[pos] * mul_by[pos] mod p (convolution)
   const uint32_t *tw_img;  // this pass's twiddle sub-table, pre-swizzled shared-memory image
@@ -593,7 +592,6 @@ static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, u
     d.C3 = ps.C3;
     d.scale_out = (inverse && ps.scale_out) ? 1 : 0;
     d.canonical_out = ps.canonical_out ? 1 : 0;
-    d.tw_stride = pl->n >> ps.logL;
     d.total_lines = batch * ps.lines_inner;
     d.mul_by = (pi + 1 == (int)pl->passes.size()) ? mul_by : nullptr;
     d.logG = ilog2_exact(ps.G);

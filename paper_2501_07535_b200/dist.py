@@ -121,6 +121,36 @@ class TorchComm:
         return out
 
 
+class SymmComm:
+    """Peer-memory exchange for the four-step (the all-to-all fused into the
+    twiddle/transpose kernel).  Every rank's receive buffer is allocated from
+    torch symmetric memory and rendezvoused, so each rank holds the NVLink
+    (peer-mapped) addresses of all receive buffers; the producing kernel
+    stores each column block straight into its destination rank's buffer and
+    a device-side barrier (stream-ordered) publishes the writes.  A barrier
+    before the stores keeps a fast rank from overwriting a buffer its peer is
+    still reading from the previous call."""
+
+    fused = True
+
+    def __init__(self, n_words: int, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        self.dist = dist
+        self.group = group if group is not None else dist.group.WORLD
+        self.rank = dist.get_rank(self.group)
+        self.world = dist.get_world_size(self.group)
+        self.recv = symm.empty(n_words, dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
+        self.handle = symm.rendezvous(self.recv, self.group.group_name)
+        self.peer_ptrs = [int(p) for p in self.handle.buffer_ptrs]
+        if len(self.peer_ptrs) != self.world:
+            raise RuntimeError("symmetric memory rendezvous returned a wrong peer count")
+
+    def barrier(self):
+        self.handle.barrier(channel=0)
+
+
 class DeviceBackend:
     """Rank-local compute on the B200 (C ABI kernels)."""
 
@@ -173,6 +203,20 @@ class DeviceBackend:
                                                     out.data_ptr(), rows, cols, stream), "wm_scale_transpose")
         return out
 
+    def scale_transpose_scatter(self, x, inverse: bool, dst_ptrs, src_rank: int):
+        """scale_transpose with the all-to-all fused in: column block d of the
+        transposed output goes straight into dst_ptrs[d] (rank d's receive
+        buffer, [P][cols/P][rows] elements) at source slot `src_rank`."""
+        rows, cols = x.shape[0], x.shape[1]
+        table = self.tw_inv if inverse else self.tw_fwd
+        P = len(dst_ptrs)
+        import ctypes
+        arr = (ctypes.c_uint64 * P)(*[int(p) for p in dst_ptrs])
+        stream = self.torch.cuda.current_stream().cuda_stream
+        self._lib.check(self.lib.wm_scale_transpose_scatter(self.field.handle, x.data_ptr(), table.data_ptr(), arr,
+                                                            P, src_rank, rows, cols, stream),
+                        "wm_scale_transpose_scatter")
+
     def block_transpose(self, x, rows: int, cols: int, block: int):
         """[rows][cols][block] -> [cols][rows][block] (block = elements)."""
         out = self.empty((cols, rows * block))
@@ -210,9 +254,28 @@ class FourStepNtt:
         return self.backend.row_ntt(e, other, inverse)
 
     def _run(self, x, inverse: bool):
+        if getattr(self.comm, "fused", False):
+            return self._run_fused(x, inverse)
         c = self.phase1(x, inverse)
         d = self.backend.empty(c.shape[:-1]) if hasattr(self.backend, "empty") else c.clone()
         self.comm.all_to_all(d, c)
+        return self.phase2(d, inverse)
+
+    def _run_fused(self, x, inverse: bool):
+        """Row NTTs, then one kernel that twiddles, transposes and stores every
+        column block into its destination rank's receive buffer (NVLink peer
+        stores), then the rank-local phase 2 on the received blocks."""
+        L = self.layout
+        P = self.world
+        row_len = L.n1 if inverse else L.n2
+        other = L.n2 if inverse else L.n1
+        y = self.backend.row_ntt(x, row_len, inverse)
+        k = self.backend.K
+        words = row_len * (other // P) * k
+        self.comm.barrier()  # every peer is done reading its receive buffer
+        self.backend.scale_transpose_scatter(y, inverse, self.comm.peer_ptrs, self.rank)
+        self.comm.barrier()  # every block has landed
+        d = self.comm.recv[:words].view(row_len, other // P, k)
         return self.phase2(d, inverse)
 
     def forward(self, x):
@@ -222,6 +285,24 @@ class FourStepNtt:
     def inverse(self, y):
         """y: [N2/P, N1, K] -> [N1/P, N2, K] (rows j1 of x)."""
         return self._run(y, True)
+
+
+def loopback_transform_fused(engines, xs, inverse: bool = False):
+    """The fused exchange over P virtual ranks on one GPU: every virtual rank's
+    receive buffer is a local tensor and the scatter kernel writes into all of
+    them (on a multi-GPU box the same kernel gets peer-mapped addresses)."""
+    import torch
+    P = len(engines)
+    L = engines[0].layout
+    row_len = L.n1 if inverse else L.n2
+    other = L.n2 if inverse else L.n1
+    k = engines[0].backend.K
+    recvs = [torch.empty((row_len, other // P, k), dtype=torch.int32, device="cuda") for _ in range(P)]
+    ptrs = [r.data_ptr() for r in recvs]
+    for r, (e, x) in enumerate(zip(engines, xs)):
+        y = e.backend.row_ntt(x, row_len, inverse)
+        e.backend.scale_transpose_scatter(y, inverse, ptrs, r)
+    return [e.phase2(d, inverse) for e, d in zip(engines, recvs)]
 
 
 def loopback_transform(engines, xs, inverse: bool = False):

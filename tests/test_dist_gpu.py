@@ -38,6 +38,84 @@ def test_loopback_four_step_matches_single_gpu(cuda, logn, P):
         assert torch.equal(back[r], xs[r])
 
 
+@pytest.mark.parametrize("logn,P", [(10, 1), (12, 4), (16, 2), (16, 8), (20, 16)])
+def test_loopback_fused_exchange_matches_nccl_form(cuda, logn, P):
+    """The all-to-all fused into the twiddle/transpose kernel (peer stores into
+    every rank's receive buffer) gives the same rank-local results as the
+    separate exchange, forward and inverse."""
+    import torch
+    from paper_2501_07535_b200 import dist as D
+    from paper_2501_07535_b200.params import find_ntt_params
+    n = 1 << logn
+    prm = find_ntt_params(256, n)
+    engines = [D.FourStepNtt(256, prm, r, P) for r in range(P)]
+    L = engines[0].layout
+    g = torch.Generator(device="cuda").manual_seed(logn + 100 * P)
+    x = torch.randint(-(1 << 31), 1 << 31, (n, 8), dtype=torch.int32, device="cuda", generator=g)
+    x[:, 7] &= (1 << 27) - 1
+    xs = [L.scatter_input(x, r) for r in range(P)]
+    ys = D.loopback_transform(engines, xs)
+    yf = D.loopback_transform_fused(engines, xs)
+    for a, b in zip(ys, yf):
+        assert torch.equal(a, b)
+    back = D.loopback_transform_fused(engines, yf, inverse=True)
+    for r in range(P):
+        assert torch.equal(back[r], xs[r])
+
+
+def test_scatter_argument_errors(cuda):
+    import torch
+    from paper_2501_07535_b200 import _lib
+    from paper_2501_07535_b200 import device as dev
+    from paper_2501_07535_b200.params import find_ntt_params
+    lib = _lib.load()
+    f = dev.Field(256, find_ntt_params(256, 1 << 10).p)
+    x = torch.zeros((4, 6, 8), dtype=torch.int32, device="cuda")
+    t = torch.zeros((4, 6, 16), dtype=torch.int32, device="cuda")
+    import ctypes
+    st = torch.cuda.current_stream().cuda_stream
+    ptrs = (ctypes.c_uint64 * 17)(*([x.data_ptr() + 4096] * 17))
+    with pytest.raises(_lib.Unsupported):  # more than 16 peers
+        _lib.check(lib.wm_scale_transpose_scatter(f.handle, x.data_ptr(), t.data_ptr(), ptrs, 17, 0, 4, 6, st))
+    with pytest.raises(ValueError):  # P does not divide cols
+        _lib.check(lib.wm_scale_transpose_scatter(f.handle, x.data_ptr(), t.data_ptr(), ptrs, 4, 0, 4, 6, st))
+    with pytest.raises(ValueError):  # source rank out of range
+        _lib.check(lib.wm_scale_transpose_scatter(f.handle, x.data_ptr(), t.data_ptr(), ptrs, 2, 2, 4, 6, st))
+
+
+def test_symmetric_memory_comm_single_rank(cuda):
+    """SymmComm plumbing (symmetric-memory rendezvous, peer pointers,
+    device barrier) on a one-rank NCCL group: the fused four-step equals the
+    single-GPU plan.  Skips where symmetric memory is unavailable."""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2501_07535_b200 import dist as D
+    from paper_2501_07535_b200 import kernels as K
+    from paper_2501_07535_b200.params import find_ntt_params
+    if dist.is_initialized():
+        pytest.skip("process group already initialised")
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29571")
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        n = 1 << 12
+        prm = find_ntt_params(256, n)
+        try:
+            comm = D.SymmComm(n * 8)
+        except Exception as exc:  # no symmetric-memory support in this torch/driver
+            pytest.skip(f"symmetric memory unavailable: {exc}")
+        eng = D.FourStepNtt(256, prm, 0, 1, comm=comm)
+        x = torch.randint(0, 1 << 27, (n, 8), dtype=torch.int32, device="cuda")
+        xl = eng.layout.scatter_input(x, 0)
+        y = eng.forward(xl)
+        want = K.get_plan(256, prm).forward(x).cpu().numpy()
+        assert np.array_equal(eng.layout.gather_output([y.cpu().numpy()]), want)
+        assert torch.equal(eng.inverse(y), xl)
+    finally:
+        dist.destroy_process_group()
+
+
 def test_transpose_kernel(cuda):
     import torch
     from paper_2501_07535_b200 import _lib
