@@ -157,12 +157,24 @@ __device__ __forceinline__ void radix4_single(uint32_t (&x0)[K], uint32_t (&x1)[
 // two at a time as radix-4 groups held in registers (one shared-memory round
 // trip and one barrier per two stages); an odd leading stage runs radix-2.
 // tww/twp[e] (e < L/2) = root_L^e and its Shoup companion.
+// Wide elements (K >= WM_NTT_RADIX2_FROM limbs) run radix-2 stages instead:
+// four K-limb values plus a twiddle pair and the Shoup temporaries exceed the
+// register file at K = 24 (spills, 1 CTA/SM); two values fit
+// (profiles/r01_ab_radix2_wide.txt: 768-bit 2^16 217 -> 101 us/transform).
+#ifndef WM_NTT_RADIX2_FROM
+#define WM_NTT_RADIX2_FROM 24
+#endif
+template <int K>
+__host__ __device__ constexpr bool ntt_radix2() {
+  return K >= WM_NTT_RADIX2_FROM;
+}
+
 template <int K>
 __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, const uint32_t *twp, int logL,
                                          int G, const NttConst<K> &c) {
   using S = Smem<K>;
   const int L = 1 << logL;
-#if defined(WM_NTT_RADIX2)
+  if constexpr (ntt_radix2<K>()) {
   for (int s = 0; s < logL; ++s) {
     const int h = 1 << s;
     for (int bf = threadIdx.x; bf < (G * L) >> 1; bf += blockDim.x) {
@@ -188,7 +200,7 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
     __syncthreads();
   }
   return;
-#endif
+  }
   int s = 0;
   if (logL & 1) {  // stage 0 alone: pairs (2m, 2m+1), twiddle 1
     for (int bf = threadIdx.x; bf < (G * L) >> 1; bf += blockDim.x) {
