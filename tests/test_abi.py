@@ -48,7 +48,7 @@ def test_host_only_entry_points(lib):
     assert lib.wm_limbs_for_bits(16) == 1
     buf = (ctypes.c_int * 32)()
     m = lib.wm_supported_limbs(1, buf, 32)
-    assert {1, 2, 4, 8, 12, 24} <= set(buf[:m])
+    assert {1, 2, 4, 8, 12, 16, 24, 32} <= set(buf[:m])
 
 
 def test_field_create_validation(lib):

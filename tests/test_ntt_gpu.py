@@ -71,7 +71,7 @@ def test_reference_2p16_checksums(cuda, golden):
         assert hashlib.sha256(yi.tobytes()).hexdigest() == row["inv_sha256"]
 
 
-@pytest.mark.parametrize("bits", [16, 32, 64, 96, 128, 192, 256, 384, 512, 768])
+@pytest.mark.parametrize("bits", [16, 32, 64, 96, 128, 192, 256, 384, 512, 768, 1024])
 @pytest.mark.parametrize("logn", [1, 2, 3, 5, 8, 10, 11, 12, 14])
 def test_sizes_and_widths_vs_c_oracle(cuda, bits, logn):
     """Every pass structure (1-3 passes) at every built width, batch 3, against
@@ -127,6 +127,32 @@ def test_2p24_properties(cuda):
     of = OracleField(prm.p, 256)
     rnd = random.Random(24)
     ks = [0, 1, n - 1, n // 2] + [rnd.randrange(n) for _ in range(4)]
+    pts = of.ntt_points(dev.to_host(x), prm.root, ks)
+    yh = dev.to_host(y)
+    for i, k in enumerate(ks):
+        assert np.array_equal(yh[k], pts[i]), k
+
+
+@pytest.mark.parametrize("bits,logn", [(512, 21), (768, 21), (1024, 19)])
+def test_wide_three_pass_properties(cuda, bits, logn):
+    """Three-pass plans at the widest limb counts (radix-2 in-smem stages at
+    24 and 32 limbs): INTT(NTT(x)) == x and random-point evaluations of the
+    forward output against the O(n) Horner oracle."""
+    dev = _dev()
+    import torch
+    n = 1 << logn
+    plan = plan_for(bits, n)
+    assert len(plan.pass_log_sizes) == 3, plan.pass_log_sizes
+    prm = plan.params
+    Kl = plan.limbs
+    g = torch.Generator(device="cuda").manual_seed(bits + logn)
+    x = torch.randint(-(1 << 31), 1 << 31, (n, Kl), dtype=torch.int32, device="cuda", generator=g)
+    x[:, Kl - 1] &= (1 << (bits - 5 - 32 * (Kl - 1))) - 1  # < 2^(bits-5) < p
+    y = plan.forward(x)
+    assert torch.equal(plan.inverse(y), x)
+    of = OracleField(prm.p, bits)
+    rnd = random.Random(bits)
+    ks = [0, 1, n - 1] + [rnd.randrange(n) for _ in range(3)]
     pts = of.ntt_points(dev.to_host(x), prm.root, ks)
     yh = dev.to_host(y)
     for i, k in enumerate(ks):
