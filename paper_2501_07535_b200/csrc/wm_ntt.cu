@@ -37,6 +37,10 @@
 #ifndef WM_NTT_MINB
 #define WM_NTT_MINB 2
 #endif
+#ifndef WM_NTT_MINB_SMALL  // K <= 4 (<= 128-bit): lighter register footprint
+#define WM_NTT_MINB_SMALL 2
+#endif
+#define WM_NTT_BOUNDS(K) __launch_bounds__(256, ((K) <= 4 ? WM_NTT_MINB_SMALL : (K) <= 12 ? WM_NTT_MINB : 1))
 // Target tile size (32-bit words of data per CTA; 16384 = 64 KB).
 #ifndef WM_NTT_TILE_WORDS
 #define WM_NTT_TILE_WORDS 16384
@@ -326,7 +330,7 @@ __global__ void twiddle_image_kernel(const uint32_t *table, int64_t stride, int 
 // ------------------------------------------------------------------ column pass
 // Line (o, i), i in [0, lines_inner) consecutive per CTA (G of them).
 template <int K>
-__global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass(const uint32_t *in, uint32_t *out,
+__global__ void WM_NTT_BOUNDS(K) ntt_col_pass(const uint32_t *in, uint32_t *out,
                                                     const uint32_t *tw_out, const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -414,7 +418,7 @@ __global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_col_pass
 // ------------------------------------------------------------------ row pass
 // Line lambda in [0, batch * lines_inner): b = lambda / R, r = lambda % R.
 template <int K>
-__global__ void __launch_bounds__(256, (K <= 12 ? WM_NTT_MINB : 1)) ntt_row_pass(const uint32_t *in, uint32_t *out,
+__global__ void WM_NTT_BOUNDS(K) ntt_row_pass(const uint32_t *in, uint32_t *out,
                                                     const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
