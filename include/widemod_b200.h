@@ -79,6 +79,13 @@ int wm_field_create(int bits, const uint32_t *q_host, int q_limbs, wm_field **ou
  * make_spec(..., strategy="karatsuba") (kernels.py:104-117, rewrite.py:234-253).
  * The NTT's Shoup multiply is a truncated product and is unaffected. */
 #define WM_FIELD_KARATSUBA 1
+/* WM_FIELD_MONTGOMERY: a full-width field — any odd q with bit length <= bits
+ * (the paper's Montgomery mode for moduli of full bit width, PAPER.md:731;
+ * e.g. secp256k1's p or BLS12-381's r at 256 bits).  Sums carry-aware,
+ * products by Montgomery multiplication (vmul: two Montgomery products, axpy:
+ * one with the scalar in Montgomery form); inputs and outputs stay canonical
+ * residues.  Built for 1, 2, 4, 8, 12, 16, 24 and 32 limbs. */
+#define WM_FIELD_MONTGOMERY 2
 int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags, wm_field **out);
 int wm_field_destroy(wm_field *f);
 int wm_field_info(const wm_field *f, int *bits, int *limbs, int *norm_shift);

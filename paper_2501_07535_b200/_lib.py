@@ -19,6 +19,7 @@ WM_ECUDA = 2
 WM_EUNSUPPORTED = 3
 WM_ELENGTH = 4
 WM_NTT_FWD, WM_NTT_INV, WM_NTT_FWD_INV, WM_NTT_COPY = 0, 1, 2, 3
+WM_FIELD_KARATSUBA, WM_FIELD_MONTGOMERY = 1, 2
 
 
 class LibraryUnavailable(RuntimeError):

@@ -46,6 +46,17 @@ bool blas_supports(int K) {
   }
 }
 
+bool mont_supports(int K) {
+  switch (K) {
+#define WM_CASE(k) case k:
+    WM_MONT_KS(WM_CASE)
+#undef WM_CASE
+    return true;
+    default:
+      return false;
+  }
+}
+
 bool ntt_supports(int K) {
   switch (K) {
 #define WM_CASE(k) case k:
@@ -121,6 +132,21 @@ Big big_pow2_div(int e, const Big &d, int limbs) {
   return quo;
 }
 
+Big big_shl_mod(const Big &a, int e, const Big &q) {
+  const int K = (int)q.size();
+  Big r = big_resize(a, K + 1), qq = big_resize(q, K + 1);
+  for (int i = 0; i < e; ++i) {
+    uint32_t carry = 0;
+    for (int j = 0; j < K + 1; ++j) {
+      const uint32_t nc = r[j] >> 31;
+      r[j] = (r[j] << 1) | carry;
+      carry = nc;
+    }
+    if (big_ge(r, qq)) big_sub_inplace(r, qq);
+  }
+  return big_resize(r, K);
+}
+
 // ------------------------------------------------------------------ field
 // ------------------------------------------------------------------ kernels
 enum BlasOp { OP_VADD = 0, OP_VSUB = 1, OP_VMUL = 2, OP_AXPY = 3 };
@@ -131,6 +157,10 @@ struct BlasArgs {
   uint32_t scal[K];  // axpy scalar, pre-shifted by F.s
 };
 
+// STRAT: kSchoolbook / kKaratsuba Barrett products, or kMontField for fields
+// with a full-width modulus (Montgomery products, carry-aware add).
+constexpr int kMontField = 2;
+
 template <int K, int OP, int STRAT>
 __global__ void __launch_bounds__(256) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
                                                    int64_t n, const __grid_constant__ BlasArgs<K> args) {
@@ -139,7 +169,19 @@ __global__ void __launch_bounds__(256) blas_kernel(const uint32_t *a, const uint
     uint32_t x[K], y[K], r[K];
     load_elem<K>(x, a, i);
     load_elem<K>(y, b, i);
-    if constexpr (OP == OP_VADD) {
+    if constexpr (STRAT == kMontField) {
+      if constexpr (OP == OP_VADD) {
+        add_mod_full<K>(r, x, y, args.F.q);
+      } else if constexpr (OP == OP_VSUB) {
+        sub_mod<K>(r, x, y, args.F.q);
+      } else if constexpr (OP == OP_VMUL) {
+        mul_mont_plain<K>(r, x, y, args.F);
+      } else {  // scal = a R mod q: one Montgomery product gives a x
+        uint32_t t[K];
+        mont_mul<K>(t, args.scal, x, args.F.q, args.F.qinv);
+        add_mod_full<K>(r, t, y, args.F.q);
+      }
+    } else if constexpr (OP == OP_VADD) {
       add_mod<K>(r, x, y, args.F.q);
     } else if constexpr (OP == OP_VSUB) {
       sub_mod<K>(r, x, y, args.F.q);
@@ -171,7 +213,8 @@ static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, 
   args.F = field_const<K>(f);
   for (int j = 0; j < K; ++j) args.scal[j] = 0;
   if (scal_host) {
-    Big sh = big_shl(Big(scal_host, scal_host + K), f->s, K);
+    const Big a(scal_host, scal_host + K);
+    const Big sh = f->mont ? to_mont(a, f->q) : big_shl(a, f->s, K);
     for (int j = 0; j < K; ++j) args.scal[j] = sh[j];
   }
   int64_t want = (n + 255) / 256;
@@ -189,6 +232,22 @@ static int blas_dispatch(int op, const wm_field *f, const uint32_t *a, const uin
   if (n == 0) return WM_OK;
   if (!a || !b || !out) return fail(WM_EINVAL, "null data pointer");
   cudaStream_t st = (cudaStream_t)stream;
+  if (f->mont) {
+    switch (f->K) {
+#define WM_CASE(k)                                                                                 \
+  case k:                                                                                          \
+    switch (op) {                                                                                  \
+      case OP_VADD: return launch_blas<k, OP_VADD, kMontField>(f, a, b, out, n, nullptr, st);      \
+      case OP_VSUB: return launch_blas<k, OP_VSUB, kMontField>(f, a, b, out, n, nullptr, st);      \
+      case OP_VMUL: return launch_blas<k, OP_VMUL, kMontField>(f, a, b, out, n, nullptr, st);      \
+      default: return launch_blas<k, OP_AXPY, kMontField>(f, a, b, out, n, scal_host, st);         \
+    }
+      WM_MONT_KS(WM_CASE)
+#undef WM_CASE
+      default:
+        return fail(WM_EUNSUPPORTED, "limb count not built into the full-width (Montgomery) kernels");
+    }
+  }
   switch (f->K) {
 #define WM_CASE(k)                                                                                 \
   case k:                                                                                          \
@@ -294,9 +353,35 @@ int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags,
   int qb = big_bitlen(q);
   const int M = 32 * K - 4;
   if (qb < 2) return fail(WM_EINVAL, "modulus must exceed 1");
+  if (flags & ~(WM_FIELD_KARATSUBA | WM_FIELD_MONTGOMERY)) return fail(WM_EINVAL, "unknown field flags");
+  if (flags & WM_FIELD_MONTGOMERY) {
+    if (flags & WM_FIELD_KARATSUBA) return fail(WM_EINVAL, "Karatsuba applies to Barrett fields only");
+    if (!mont_supports(K)) return fail(WM_EUNSUPPORTED, "width not built into the full-width (Montgomery) kernels");
+    if (!(q[0] & 1u)) return fail(WM_EINVAL, "full-width (Montgomery) fields need an odd modulus");
+    if (qb > bits) return fail(WM_EINVAL, "modulus wider than the field width");
+    if (qb < 3) return fail(WM_EINVAL, "modulus must exceed 2");
+    wm_field *f = new wm_field();
+    f->mont = true;
+    f->bits = bits;
+    f->K = K;
+    f->s = 0;
+    f->q = q;
+    Big zero(K, 0u);
+    f->qn = q;
+    f->qn2 = zero;
+    f->nqn = zero;
+    f->mu8 = zero;
+    uint32_t x = q[0];  // Newton: inverse of q mod 2^32 (x = q is correct mod 8)
+    for (int i = 0; i < 4; ++i) x *= 2u - q[0] * x;
+    f->qinv = 0u - x;
+    Big one(K, 0u);
+    one[0] = 1;
+    f->r2 = big_shl_mod(one, 64 * K, q);
+    *out = f;
+    return WM_OK;
+  }
   if (qb > M) return fail(WM_EINVAL, "modulus must be below 2^(32K-4)");
   if (M - qb > 31) return fail(WM_EINVAL, "modulus too small for the field width (normalisation shift > 31)");
-  if (flags & ~WM_FIELD_KARATSUBA) return fail(WM_EINVAL, "unknown field flags");
   wm_field *f = new wm_field();
   f->karatsuba = (flags & WM_FIELD_KARATSUBA) != 0;
   f->bits = bits;

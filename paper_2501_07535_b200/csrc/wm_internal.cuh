@@ -38,12 +38,17 @@ int cuda_fail(cudaError_t e, const char *what);
 #ifndef WM_BLAS_KS
 #define WM_BLAS_KS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(16) X(24) X(32)
 #endif
+// Full-width (Montgomery) fields: the common curve / FHE sizes.
+#ifndef WM_MONT_KS
+#define WM_MONT_KS(X) X(1) X(2) X(4) X(8) X(12) X(16) X(24) X(32)
+#endif
 #ifndef WM_NTT_KS
 #define WM_NTT_KS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(12) X(16) X(24) X(32)
 #endif
 
 bool blas_supports(int K);
 bool ntt_supports(int K);
+bool mont_supports(int K);
 
 // ------------------------------------------------------------------ host bignum
 using Big = std::vector<uint32_t>;  // little-endian limbs, fixed length
@@ -54,12 +59,19 @@ void big_sub_inplace(Big &a, const Big &b);            // a -= b, same length, a
 Big big_resize(const Big &a, int limbs);
 // floor(2^e / d) truncated to `limbs` limbs (binary long division).
 Big big_pow2_div(int e, const Big &d, int limbs);
+// (a * 2^e) mod q, a < q, K = q.size() limbs.
+Big big_shl_mod(const Big &a, int e, const Big &q);
+// Montgomery form a * 2^(32K) mod q.
+inline Big to_mont(const Big &a, const Big &q) { return big_shl_mod(a, 32 * (int)q.size(), q); }
 
 // ------------------------------------------------------------------ objects
 }  // namespace wm
 
 struct wm_field {
   bool karatsuba = false;  // vmul/axpy use the Karatsuba full product
+  bool mont = false;       // full-width modulus, Montgomery arithmetic (WM_FIELD_MONTGOMERY)
+  uint32_t qinv = 0;       // mont: -q^-1 mod 2^32
+  wm::Big r2;              // mont: 2^(64K) mod q
   int bits = 0;
   int K = 0;
   int s = 0;
@@ -127,8 +139,10 @@ inline FieldConst<K> field_const(const wm_field *f) {
     c.qn2[j] = f->qn2[j];
     c.nqn[j] = f->nqn[j];
     c.mu8[j] = f->mu8[j];
+    c.r2[j] = f->mont ? f->r2[j] : 0u;
   }
   c.s = (uint32_t)f->s;
+  c.qinv = f->qinv;
   return c;
 }
 

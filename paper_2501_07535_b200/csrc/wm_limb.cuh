@@ -516,6 +516,8 @@ __device__ void shoup_companion_dev(uint32_t (&wp)[K], const uint32_t (&w)[K], c
 template <int K>
 struct FieldConst {
   uint32_t q[K];    // the modulus (canonical-residue bound)
+  uint32_t r2[K];   // Montgomery fields: 2^(64K) mod q
+  uint32_t qinv;    // Montgomery fields: -q^-1 mod 2^32
   uint32_t qn[K];   // q << s
   uint32_t qn2[K];  // 2 * qn
   uint32_t nqn[K];  // 2^(32K) - qn
@@ -581,6 +583,74 @@ WM_DEV void mul_barrett(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t
   uint32_t as[K];
   shl_small<K>(as, a, F.s);
   mul_barrett_pre<K, barrett_style<K>(), STRAT>(r, as, b, F);
+}
+
+// ------------------------------------------------------------------ full-width moduli
+// Fields created with WM_FIELD_MONTGOMERY take any odd q < 2^(32K) (the
+// paper's full-width mode; the reference and the Barrett path
+// need q < 2^(32K-4)).  Sums can carry out of K limbs, so the modular add
+// looks at the carry; products use Montgomery multiplication.
+
+// r = a + b mod q for canonical a, b and any q < 2^(32K).
+template <int K>
+WM_DEV void add_mod_full(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K], const uint32_t (&q)[K]) {
+  uint32_t s[K], d[K];
+  const uint32_t c = add_n<K>(s, a, b);
+  const uint32_t br = sub_n<K>(d, s, q);
+  // s + c 2^32K >= q  <=>  carry out of the sum, or no borrow from s - q
+  select_n<K>(r, c | (br ^ 0xffffffffu), d, s);
+}
+
+// Montgomery product r = a b 2^(-32K) mod q (CIOS: interleaved row product
+// and row reduction; 2K^2 + K word products), odd q < 2^(32K), a, b < q,
+// canonical output.  qinv = -q^-1 mod 2^32.
+template <int K>
+WM_DEV void mont_mul(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K], const uint32_t (&q)[K],
+                     uint32_t qinv) {
+  uint32_t t[K + 2];
+#pragma unroll
+  for (int j = 0; j < K + 2; ++j) t[j] = 0u;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint64_t p = (uint64_t)a[j] * b[i] + t[j] + c;
+      t[j] = (uint32_t)p;
+      c = (uint32_t)(p >> 32);
+    }
+    uint64_t sK = (uint64_t)t[K] + c;
+    t[K] = (uint32_t)sK;
+    t[K + 1] = (uint32_t)(sK >> 32);
+    const uint32_t m = t[0] * qinv;
+    uint64_t p = (uint64_t)m * q[0] + t[0];
+    c = (uint32_t)(p >> 32);
+#pragma unroll
+    for (int j = 1; j < K; ++j) {
+      p = (uint64_t)m * q[j] + t[j] + c;
+      t[j - 1] = (uint32_t)p;
+      c = (uint32_t)(p >> 32);
+    }
+    sK = (uint64_t)t[K] + c;
+    t[K - 1] = (uint32_t)sK;
+    t[K] = t[K + 1] + (uint32_t)(sK >> 32);
+  }
+  // t < 2q: one conditional subtraction (t[K] is the carry limb)
+  uint32_t lo[K], d[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) lo[j] = t[j];
+  const uint32_t br = sub_n<K>(d, lo, q);
+  select_n<K>(r, t[K] | (br ^ 0xffffffffu), d, lo);
+}
+
+// a b mod q for a Montgomery field: two Montgomery products (a b R^-1, then
+// times R^2 R^-1).
+template <int K>
+WM_DEV void mul_mont_plain(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K],
+                           const FieldConst<K> &F) {
+  uint32_t t[K];
+  mont_mul<K>(t, a, b, F.q, F.qinv);
+  mont_mul<K>(r, t, F.r2, F.q, F.qinv);
 }
 
 }  // namespace wm

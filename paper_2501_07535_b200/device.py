@@ -89,7 +89,7 @@ class Field:
         self.lib = _lib.load()
         self.bits = int(bits)
         self.q = int(q)
-        if strategy not in ("schoolbook", "karatsuba"):
+        if strategy not in ("schoolbook", "karatsuba", "montgomery"):
             raise ValueError(f"unknown multiplication strategy {strategy!r}")
         self.strategy = strategy
         self.limbs = limbs_for_bits(self.bits)
@@ -98,7 +98,10 @@ class Field:
         ql = ints_to_limbs([self.q], self.limbs)[0]
         arr = _lib.u32_array(ql.tolist())
         h = ctypes.c_void_p()
-        flags = 1 if strategy == "karatsuba" else 0
+        # "montgomery": full-width modulus (any odd q < 2^bits), Montgomery
+        # products (the paper's full-width mode)
+        flags = {"schoolbook": 0, "karatsuba": _lib.WM_FIELD_KARATSUBA,
+                 "montgomery": _lib.WM_FIELD_MONTGOMERY}[strategy]
         _lib.check(self.lib.wm_field_create_ex(self.bits, arr, self.limbs, flags, ctypes.byref(h)),
                    "wm_field_create_ex")
         self._h = h
