@@ -239,6 +239,7 @@ def run_gpu(args, rank, world, local, pg):
     four = run_four_step(args, torch, rank, world, pg) if not args.skip_extras else None
     b20 = run_batched_2p20(args, torch, rank, world, pg) if not args.skip_extras else None
     refgpu = run_reference_gpu(args, torch, plan) if (world == 1 and not args.skip_extras) else None
+    fullw = run_full_width(args, torch) if not args.skip_extras else None
 
     return {
         "us_per_transform": us_per_transform,
@@ -252,6 +253,7 @@ def run_gpu(args, rank, world, local, pg):
         "four_step": four,
         "batched_2p20": b20,
         "reference_gpu": refgpu,
+        "full_width": fullw,
     }
 
 
@@ -453,6 +455,52 @@ def run_four_step_fused(torch, prm, rank, world, pg, x, y_ref, reps):
     finally:
         if own_group:
             dist.destroy_process_group()
+
+
+def run_full_width(args, torch):
+    """Full-width field (WM_FIELD_MONTGOMERY, the paper's Montgomery mode,
+    PAPER.md:731): the BLS12-381 scalar field r (255 bits, outside the
+    reference's q < 2^(bits-4) range) at 256 bits — NTT n=2^16 batch 64
+    fwd+inv and vadd/vmul/axpy at n=2^24."""
+    from paper_2501_07535_b200 import device as dev
+    from paper_2501_07535_b200.params import NttParams
+    r = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+    f = dev.Field(256, r, "montgomery")
+    g = 7  # multiplicative generator of F_r
+    root = pow(g, (r - 1) // N, r)
+    plan = dev.NttPlan(f, NttParams(n=N, p=r, root=root, root_inv=pow(root, -1, r), n_inv=pow(N, -1, r)))
+    x = canonical_random(torch, BATCH * N, 555)
+    y, z = torch.empty_like(x), torch.empty_like(x)
+    ws = torch.empty(plan.workspace_bytes(BATCH) // 4, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, reps=10):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(reps)]
+        for e0, e1 in evs:
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+        torch.cuda.synchronize()
+        return statistics.median(a.elapsed_time(b) for a, b in evs)
+
+    ms = timed(lambda: (plan.forward(x, out=y, workspace=ws), plan.inverse(y, out=z, workspace=ws)))
+    assert torch.equal(z, x), "full-width NTT roundtrip mismatch"
+    res = {"field": "BLS12-381 r (255-bit), 256-bit interface width, Montgomery",
+           "ntt_2p16_us_per_transform": round(ms * 1e3 / (2 * BATCH), 3)}
+    del x, y, z, ws
+    m = 1 << 24
+    a = canonical_random(torch, m, 11)
+    b = canonical_random(torch, m, 12)
+    o = torch.empty_like(a)
+    for op in ("vadd", "vmul", "axpy"):
+        fn = (lambda: f.axpy(12345, a, b, out=o)) if op == "axpy" else (lambda op=op: getattr(f, op)(a, b, out=o))
+        res[f"{op}_2p24_GBps"] = round(3 * 4 * K_LIMBS * m / (timed(fn) * 1e-3) / 1e9, 1)
+    del a, b, o
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_batched_2p20(args, torch, rank, world, pg):
@@ -782,6 +830,7 @@ def main():
         "four_step_2p24": res["four_step"],
         "batched_2p20_x256": res["batched_2p20"],
         "reference_gpu": res["reference_gpu"],
+        "full_width_bls12_381": res["full_width"],
     }
     emit(out)
     if pg is not None:

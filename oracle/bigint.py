@@ -184,6 +184,41 @@ def run_ntt(values: list[int], prm: dict, width: int, inverse: bool = False) -> 
     return x
 
 
+def run_ntt_exact(values: list[int], p: int, root: int, n_inv: int, inverse: bool = False) -> list[int]:
+    """run_ntt (kernels.py:483-499) with exact modular products instead of the
+    reference's width-bound Barrett: the same bit-reversal, butterfly schedule
+    and inverse scaling, valid for any prime p (full-width moduli, which the
+    reference's compute_barrett range excludes).  `root` is root_inv for the
+    inverse; agrees with run_ntt wherever both apply (tests/test_oracle_pinned.py)."""
+    n = len(values)
+    tw = [pow(root, e, p) for e in range(n // 2)]
+    rev = bit_reverse_order(n)
+    x = [values[rev[i]] for i in range(n)]
+    m = 2
+    while m <= n:
+        half, step = m // 2, n // m
+        for base in range(0, n, m):
+            for j in range(half):
+                u, v = x[base + j], x[base + j + half]
+                t = v * tw[j * step] % p
+                x[base + j] = (u + t) % p
+                x[base + j + half] = (u - t) % p
+        m *= 2
+    if inverse:
+        x = [v * n_inv % p for v in x]
+    return x
+
+
+def ntt_point(values: list[int], p: int, root: int, k: int) -> int:
+    """y[k] = sum_j x[j] root^(jk) mod p by Horner (the DFT ntt_reference,
+    oracle.py:262-282, at one output index)."""
+    w = pow(root, k, p)
+    acc = 0
+    for x in reversed(values):
+        acc = (acc * w + x) % p
+    return acc
+
+
 # ------------------------------------------------------------ inputs (SURVEY §8(d))
 def uniform_residues(rng: np.random.Generator, count: int, q: int) -> list[int]:
     """Uniform values in [0, q): k uint32 limbs per value, top limb masked to

@@ -239,6 +239,7 @@ int wm_transpose(int words, const uint32_t *in, uint32_t *out, int64_t rows, int
 
 int wm_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out, int64_t rows,
                        int64_t cols, void *stream) {
+  if (f && f->mont) return fail(WM_EUNSUPPORTED, "the distributed four-step supports reference-range (Barrett) fields only");
   if (!f) return fail(WM_EINVAL, "null field");
   if (rows < 0 || cols < 0) return fail(WM_EINVAL, "bad shape");
   if (rows == 0 || cols == 0) return WM_OK;
@@ -259,6 +260,7 @@ int wm_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *ta
 int wm_scale_transpose_scatter(const wm_field *f, const uint32_t *in, const uint32_t *table,
                                const uint64_t *dst_ptrs, int P, int src_rank, int64_t rows, int64_t cols,
                                void *stream) {
+  if (f && f->mont) return fail(WM_EUNSUPPORTED, "the distributed four-step supports reference-range (Barrett) fields only");
   if (!f) return fail(WM_EINVAL, "null field");
   if (rows < 0 || cols < 0) return fail(WM_EINVAL, "bad shape");
   if (P < 1 || P > kMaxPeers) return fail(WM_EUNSUPPORTED, "peer count outside 1..16");
@@ -289,6 +291,7 @@ int wm_scale_transpose_scatter(const wm_field *f, const uint32_t *in, const uint
 
 int wm_twiddle_table_2d(const wm_field *f, int64_t n, const uint32_t *root_host, int64_t row0, int64_t rows,
                         int64_t cols, uint32_t *table, void *stream) {
+  if (f && f->mont) return fail(WM_EUNSUPPORTED, "the distributed four-step supports reference-range (Barrett) fields only");
   if (!f || !root_host || !table) return fail(WM_EINVAL, "null argument");
   if (n < 1 || (n & (n - 1)) || rows < 0 || cols < 0 || row0 < 0) return fail(WM_EINVAL, "bad shape");
   if (rows == 0 || cols == 0) return WM_OK;

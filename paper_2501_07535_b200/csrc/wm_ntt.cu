@@ -78,6 +78,72 @@ struct PassDesc {
   int logG, logn, log_inner, log_tiles_inner, logRT, logWK, logWO;
 };
 
+// ------------------------------------------------------------------ arithmetic policy
+// MONT = false: reference-range fields (p < 2^(32K-4)): Shoup twiddle
+// products (tables hold (w, w')), lazy values in [0, 6p), canonical at the end.
+// MONT = true: full-width fields (WM_FIELD_MONTGOMERY, any odd p < 2^(32K)):
+// tables hold w R mod p, each product is a Montgomery product, values stay
+// canonical (no headroom above p for a lazy window).
+template <int K, bool MONT>
+struct Arith;
+
+template <int K>
+struct Arith<K, false> {
+  static constexpr bool kWp = true;
+  WM_DEV static void bf(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&wp)[K],
+                        const NttConst<K> &c) {
+    bf_lazy<K>(x0, x1, w, wp, c.p3, c.np);
+  }
+  WM_DEV static void bf1(uint32_t (&x0)[K], uint32_t (&x1)[K], const NttConst<K> &c) { bf_lazy_w1<K>(x0, x1, c.p3); }
+  WM_DEV static void twmul(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
+                           const uint32_t (&wp)[K], const NttConst<K> &c) {
+    mul_shoup_lazy<K>(r, v, w, wp, c.np);
+  }
+  WM_DEV static void canon(uint32_t (&v)[K], const NttConst<K> &c) { canonical_6p<K>(v, c.p, c.p2, c.p4); }
+  WM_DEV static void mulby(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&m)[K], const NttConst<K> &c) {
+    mul_barrett<K>(r, v, m, c.F);
+  }
+};
+
+template <int K>
+struct Arith<K, true> {
+  static constexpr bool kWp = false;
+  WM_DEV static void finish(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&t)[K], const NttConst<K> &c) {
+    uint32_t a[K], b[K];
+    add_mod_full<K>(a, x0, t, c.p);
+    sub_mod<K>(b, x0, t, c.p);
+    copy_n<K>(x0, a);
+    copy_n<K>(x1, b);
+  }
+  WM_DEV static void bf(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&)[K],
+                        const NttConst<K> &c) {
+    uint32_t t[K];
+    mont_mul<K>(t, x1, w, c.p, c.F.qinv);
+    finish(x0, x1, t, c);
+  }
+  WM_DEV static void bf1(uint32_t (&x0)[K], uint32_t (&x1)[K], const NttConst<K> &c) {
+    uint32_t t[K];
+    copy_n<K>(t, x1);
+    finish(x0, x1, t, c);
+  }
+  WM_DEV static void twmul(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
+                           const uint32_t (&)[K], const NttConst<K> &c) {
+    mont_mul<K>(r, v, w, c.p, c.F.qinv);
+  }
+  WM_DEV static void canon(uint32_t (&)[K], const NttConst<K> &) {}
+  WM_DEV static void mulby(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&m)[K], const NttConst<K> &c) {
+    mul_mont_plain<K>(r, v, m, c.F);
+  }
+};
+
+// Limb counts with a full-width (Montgomery) NTT instantiation.
+template <int K>
+__host__ __device__ constexpr bool mont_ntt_built() {
+#define WM_EQ(k) || K == k
+  return false WM_MONT_KS(WM_EQ);
+#undef WM_EQ
+}
+
 // ------------------------------------------------------------------ smem layout
 // Element e of the CTA's tile occupies K words.  When K is a multiple of 4 and
 // K/4 a power of two, an element is C = K/4 16-byte chunks and chunk (e, c)
@@ -128,32 +194,33 @@ struct Smem {
 // ------------------------------------------------------------------ in-smem DFT
 // One radix-4 group (stages s, s+1) with one product at a time (wide K,
 // where two interleaved products would spill registers).
-template <int K>
+template <int K, bool MONT>
 __device__ __forceinline__ void radix4_single(uint32_t (&x0)[K], uint32_t (&x1)[K], uint32_t (&x2)[K],
                                               uint32_t (&x3)[K], const uint32_t *tww, const uint32_t *twp, int s,
                                               int j, int h, int logL, int lq, bool trivial,
                                               const NttConst<K> &c) {
   using S = Smem<K>;
+  using A = Arith<K, MONT>;
   uint32_t w[K], wp[K];
   if (trivial) {  // j == 0: the stage-s twiddle and the first stage-(s+1) twiddle are 1
-    bf_lazy_w1<K>(x0, x1, c.p3);
-    bf_lazy_w1<K>(x2, x3, c.p3);
-    bf_lazy_w1<K>(x0, x2, c.p3);  // j = 0: root^0
+    A::bf1(x0, x1, c);
+    A::bf1(x2, x3, c);
+    A::bf1(x0, x2, c);  // j = 0: root^0
   } else {
     const int i1 = j << (logL - 1 - s);
     S::load(w, tww, i1);
-    S::load(wp, twp, i1);
-    bf_lazy<K>(x0, x1, w, wp, c.p3, c.np);
-    bf_lazy<K>(x2, x3, w, wp, c.p3, c.np);
+    if constexpr (A::kWp) S::load(wp, twp, i1);
+    A::bf(x0, x1, w, wp, c);
+    A::bf(x2, x3, w, wp, c);
     const int i2 = j << (lq - s);
     S::load(w, tww, i2);
-    S::load(wp, twp, i2);
-    bf_lazy<K>(x0, x2, w, wp, c.p3, c.np);
+    if constexpr (A::kWp) S::load(wp, twp, i2);
+    A::bf(x0, x2, w, wp, c);
   }
   const int i3 = (j + h) << (lq - s);
   S::load(w, tww, i3);
-  S::load(wp, twp, i3);
-  bf_lazy<K>(x1, x3, w, wp, c.p3, c.np);
+  if constexpr (A::kWp) S::load(wp, twp, i3);
+  A::bf(x1, x3, w, wp, c);
 }
 
 // G lines of L = 2^logL elements (tile element g*L + pos), bit-reversed order
@@ -173,10 +240,11 @@ __host__ __device__ constexpr bool ntt_radix2() {
   return K >= WM_NTT_RADIX2_FROM;
 }
 
-template <int K>
+template <int K, bool MONT>
 __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, const uint32_t *twp, int logL,
                                          int G, const NttConst<K> &c) {
   using S = Smem<K>;
+  using A = Arith<K, MONT>;
   const int L = 1 << logL;
   if constexpr (ntt_radix2<K>()) {
   for (int s = 0; s < logL; ++s) {
@@ -190,13 +258,13 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
       S::load(x0, data, e0);
       S::load(x1, data, e0 + h);
       if (s == 0) {
-        bf_lazy_w1<K>(x0, x1, c.p3);
+        A::bf1(x0, x1, c);
       } else {
         uint32_t w[K], wp[K];
         const int i1 = j << (logL - 1 - s);
         S::load(w, tww, i1);
-        S::load(wp, twp, i1);
-        bf_lazy<K>(x0, x1, w, wp, c.p3, c.np);
+        if constexpr (A::kWp) S::load(wp, twp, i1);
+        A::bf(x0, x1, w, wp, c);
       }
       S::store(data, e0, x0);
       S::store(data, e0 + h, x1);
@@ -212,7 +280,7 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
       uint32_t x0[K], x1[K];
       S::load(x0, data, e0);
       S::load(x1, data, e0 + 1);
-      bf_lazy_w1<K>(x0, x1, c.p3);
+      A::bf1(x0, x1, c);
       S::store(data, e0, x0);
       S::store(data, e0 + 1, x1);
     }
@@ -249,7 +317,7 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
       S::load(x1, data, e0 + h);
       S::load(x2, data, e0 + 2 * h);
       S::load(x3, data, e0 + 3 * h);
-      radix4_single<K>(x0, x1, x2, x3, tww, twp, s, j, h, logL, lq, s == 0 || (jmajor && j == 0), c);
+      radix4_single<K, MONT>(x0, x1, x2, x3, tww, twp, s, j, h, logL, lq, s == 0 || (jmajor && j == 0), c);
 
       S::store(data, e0, x0);
       S::store(data, e0 + h, x1);
@@ -329,7 +397,7 @@ __global__ void twiddle_image_kernel(const uint32_t *table, int64_t stride, int 
 
 // ------------------------------------------------------------------ column pass
 // Line (o, i), i in [0, lines_inner) consecutive per CTA (G of them).
-template <int K>
+template <int K, bool MONT>
 __global__ void WM_NTT_BOUNDS(K) ntt_col_pass(const uint32_t *in, uint32_t *out,
                                                     const uint32_t *tw_out, const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
@@ -372,7 +440,7 @@ __global__ void WM_NTT_BOUNDS(K) ntt_col_pass(const uint32_t *in, uint32_t *out,
   }
   __syncthreads();
   twimg_wait(mbar);
-  dft_smem<K>(data, tww, twp, logL, G, c);
+  dft_smem<K, MONT>(data, tww, twp, logL, G, c);
   // inter-pass twiddle exponent, reduced mod n (n | 2^32, so 32-bit wraparound is exact)
   const uint32_t nmask = (uint32_t)(d.n - 1);
   const uint32_t oc1 = (uint32_t)(o * d.C1);
@@ -387,7 +455,7 @@ __global__ void WM_NTT_BOUNDS(K) ntt_col_pass(const uint32_t *in, uint32_t *out,
         const uint32_t e = ((uint32_t)((i0 + g) >> d.SH) * (oc1 + (uint32_t)k * (uint32_t)d.C2) *
                             (uint32_t)d.C3) & nmask;
         ldg_elem<K>(w[u], tw_out + (size_t)e * (2 * K));
-        ldg_elem<K>(wp[u], tw_out + (size_t)e * (2 * K) + K);
+        if constexpr (Arith<K, MONT>::kWp) ldg_elem<K>(wp[u], tw_out + (size_t)e * (2 * K) + K);
       }
     }
 #pragma unroll
@@ -399,15 +467,15 @@ __global__ void WM_NTT_BOUNDS(K) ntt_col_pass(const uint32_t *in, uint32_t *out,
       S::load(v, data, g * L + k);
       if (d.C3) {
         uint32_t r[K];
-        mul_shoup_lazy<K>(r, v, w[u], wp[u], c.np);
+        Arith<K, MONT>::twmul(r, v, w[u], wp[u], c);
         copy_n<K>(v, r);
       }
-      if (d.canonical_out) canonical_6p<K>(v, c.p, c.p2, c.p4);
+      if (d.canonical_out) Arith<K, MONT>::canon(v, c);
       const int64_t off = (((int64_t)k << d.logWK) + g) * K;
       if (d.mul_by) {
         uint32_t m[K], rr[K];
         ldg_elem<K>(m, d.mul_by + (dst - out) + off);
-        mul_barrett<K>(rr, v, m, c.F);
+        Arith<K, MONT>::mulby(rr, v, m, c);
         copy_n<K>(v, rr);
       }
       stg_elem<K>(dst + off, v);
@@ -417,7 +485,7 @@ __global__ void WM_NTT_BOUNDS(K) ntt_col_pass(const uint32_t *in, uint32_t *out,
 
 // ------------------------------------------------------------------ row pass
 // Line lambda in [0, batch * lines_inner): b = lambda / R, r = lambda % R.
-template <int K>
+template <int K, bool MONT>
 __global__ void WM_NTT_BOUNDS(K) ntt_row_pass(const uint32_t *in, uint32_t *out,
                                                     const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
@@ -454,7 +522,7 @@ __global__ void WM_NTT_BOUNDS(K) ntt_row_pass(const uint32_t *in, uint32_t *out,
   }
   __syncthreads();
   twimg_wait(mbar);
-  dft_smem<K>(data, tww, twp, logL, G, c);
+  dft_smem<K, MONT>(data, tww, twp, logL, G, c);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
     const int g = idx >> logL, k = idx & (L - 1);
     const int64_t lam = lam0 + g;
@@ -464,15 +532,15 @@ __global__ void WM_NTT_BOUNDS(K) ntt_row_pass(const uint32_t *in, uint32_t *out,
       S::load(v, data, g * L + k);
       if (d.scale_out) {
         uint32_t rr[K];
-        mul_shoup_lazy<K>(rr, v, c.sc, c.scp, c.np);
+        Arith<K, MONT>::twmul(rr, v, c.sc, c.scp, c);
         copy_n<K>(v, rr);
       }
-      if (d.canonical_out) canonical_6p<K>(v, c.p, c.p2, c.p4);
+      if (d.canonical_out) Arith<K, MONT>::canon(v, c);
       const int64_t pos = (b << d.logn) + (r << d.logWO) + ((int64_t)k << d.logWK);
       if (d.mul_by) {  // fused pointwise product (NTT-domain convolution)
         uint32_t m[K], rr[K];
         ldg_elem<K>(m, d.mul_by + pos * K);
-        mul_barrett<K>(rr, v, m, c.F);
+        Arith<K, MONT>::mulby(rr, v, m, c);
         copy_n<K>(v, rr);
       }
       stg_elem<K>(out + pos * K, v);
@@ -489,7 +557,14 @@ struct TwGenArgs {
   int64_t chunk;
 };
 
-template <int K>
+// MONT: base and scale arrive in Montgomery form and every product is a
+// Montgomery product, so the table holds root^e * R mod p (no companion).
+template <int K, bool MONT>
+WM_DEV void tw_mul(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K], const FieldConst<K> &F) {
+  if constexpr (MONT) mont_mul<K>(r, a, b, F.q, F.qinv); else mul_barrett<K>(r, a, b, F);
+}
+
+template <int K, bool MONT>
 __global__ void twiddle_gen_kernel(uint32_t *table, int64_t count, const __grid_constant__ TwGenArgs<K> a) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t e0 = t * a.chunk;
@@ -500,30 +575,38 @@ __global__ void twiddle_gen_kernel(uint32_t *table, int64_t count, const __grid_
   for (int64_t e = e0; e; e >>= 1) {
     uint32_t r[K];
     if (e & 1) {
-      mul_barrett<K>(r, x, b, a.F);
+      tw_mul<K, MONT>(r, x, b, a.F);
       copy_n<K>(x, r);
     }
-    mul_barrett<K>(r, b, b, a.F);
+    tw_mul<K, MONT>(r, b, b, a.F);
     copy_n<K>(b, r);
   }
   const int64_t e1 = (e0 + a.chunk < count) ? e0 + a.chunk : count;
   for (int64_t e = e0; e < e1; ++e) {
     uint32_t wp[K];
-    shoup_companion_dev<K>(wp, x, a.F.q);
+    if constexpr (MONT) zero_n<K>(wp); else shoup_companion_dev<K>(wp, x, a.F.q);
     stg_elem<K>(table + e * (2 * K), x);
     stg_elem<K>(table + e * (2 * K) + K, wp);
     uint32_t r[K];
-    mul_barrett<K>(r, x, a.base, a.F);
+    tw_mul<K, MONT>(r, x, a.base, a.F);
     copy_n<K>(x, r);
   }
 }
 
-template <int K>
-__global__ void twiddle_extract_kernel(const uint32_t *table, int64_t count, uint32_t *out) {
+template <int K, bool MONT>
+__global__ void twiddle_extract_kernel(const uint32_t *table, int64_t count, uint32_t *out,
+                                       const __grid_constant__ FieldConst<K> F) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += stride) {
     uint32_t v[K];
     ldg_elem<K>(v, table + e * (2 * K));
+    if constexpr (MONT) {  // w R -> w
+      uint32_t one[K], r[K];
+      zero_n<K>(one);
+      one[0] = 1u;
+      mont_mul<K>(r, v, one, F.q, F.qinv);
+      copy_n<K>(v, r);
+    }
     for (int j = 0; j < K; ++j) out[e * K + j] = v[j];
   }
 }
@@ -534,14 +617,23 @@ template <int K>
 static int gen_table(const wm_field *f, uint32_t *table, int64_t count, const Big &base, const Big &scale) {
   TwGenArgs<K> a;
   a.F = field_const<K>(f);
+  const Big bm = f->mont ? to_mont(base, f->q) : base, sm = f->mont ? to_mont(scale, f->q) : scale;
   for (int j = 0; j < K; ++j) {
-    a.base[j] = base[j];
-    a.scale[j] = scale[j];
+    a.base[j] = bm[j];
+    a.scale[j] = sm[j];
   }
   a.chunk = 64;
   int64_t threads = (count + a.chunk - 1) / a.chunk;
   int grid = (int)((threads + 127) / 128);
-  twiddle_gen_kernel<K><<<grid, 128>>>(table, count, a);
+  if constexpr (mont_ntt_built<K>()) {
+    if (f->mont) {
+      twiddle_gen_kernel<K, true><<<grid, 128>>>(table, count, a);
+      WM_LAUNCH_CHECK("twiddle_gen launch");
+      return WM_OK;
+    }
+  }
+  if (f->mont) return fail(WM_EUNSUPPORTED, "limb count not built into the full-width NTT kernels");
+  twiddle_gen_kernel<K, false><<<grid, 128>>>(table, count, a);
   WM_LAUNCH_CHECK("twiddle_gen launch");
   return WM_OK;
 }
@@ -556,7 +648,7 @@ static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
     c.p3[j] = pl->p3[j];
     c.p4[j] = pl->p4[j];
     c.np[j] = pl->np[j];
-    c.sc[j] = pl->ninv[j];
+    c.sc[j] = pl->field->mont ? pl->ninv_mont[j] : pl->ninv[j];
     c.scp[j] = pl->ninv_sh[j];
   }
   return c;
@@ -572,14 +664,13 @@ static size_t pass_smem(int K, const wm_pass_plan &ps) {
   return round4_h((size_t)ps.G * L * K) * sizeof(uint32_t) + twimg_bytes(K, ps.logL) + 16;  // + mbarrier
 }
 
-template <int K>
-static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
-                      uint32_t *ws, cudaStream_t st, int only_pass = -1,
-                      const uint32_t *mul_by = nullptr) {
+template <int K, bool MONT>
+static int run_passes_t(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
+                        uint32_t *ws, cudaStream_t st, int only_pass, const uint32_t *mul_by) {
   static bool attr_done = false;
   if (!attr_done) {
-    WM_CUDA_TRY(cudaFuncSetAttribute(ntt_col_pass<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    WM_CUDA_TRY(cudaFuncSetAttribute(ntt_row_pass<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    WM_CUDA_TRY(cudaFuncSetAttribute(ntt_col_pass<K, MONT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    WM_CUDA_TRY(cudaFuncSetAttribute(ntt_row_pass<K, MONT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_done = true;
   }
   const NttConst<K> c = ntt_const<K>(pl);
@@ -622,16 +713,26 @@ static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, u
     if (ps.column) {
       const uint32_t *tw_out = inverse ? (ps.scaled_table ? pl->tw_inv_scaled : pl->tw_inv) : pl->tw_fwd;
       dim3 grid((unsigned)(ps.lines_outer * (ps.lines_inner / ps.G)), (unsigned)batch);
-      ntt_col_pass<K><<<grid, 256, smem, st>>>(src, dst, tw_out, d, c);
+      ntt_col_pass<K, MONT><<<grid, 256, smem, st>>>(src, dst, tw_out, d, c);
       WM_LAUNCH_CHECK("ntt_col_pass launch");
     } else {
       const int64_t lines = batch * ps.lines_inner;
       dim3 grid((unsigned)((lines + ps.G - 1) / ps.G));
-      ntt_row_pass<K><<<grid, 256, smem, st>>>(src, dst, d, c);
+      ntt_row_pass<K, MONT><<<grid, 256, smem, st>>>(src, dst, d, c);
       WM_LAUNCH_CHECK("ntt_row_pass launch");
     }
   }
   return WM_OK;
+}
+
+template <int K>
+static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
+                      uint32_t *ws, cudaStream_t st, int only_pass = -1, const uint32_t *mul_by = nullptr) {
+  if constexpr (mont_ntt_built<K>()) {
+    if (pl->field->mont) return run_passes_t<K, true>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);
+  }
+  if (pl->field->mont) return fail(WM_EUNSUPPORTED, "limb count not built into the full-width NTT kernels");
+  return run_passes_t<K, false>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);
 }
 
 static int plan_passes(wm_ntt_plan *pl) {
@@ -814,6 +915,8 @@ int wm_ntt_plan_create(const wm_field *f, int64_t n, const uint32_t *root_host, 
   if (n > ((int64_t)1 << 30)) return fail(WM_EUNSUPPORTED, "transform length above 2^30");
   const int K = f->K;
   if (!ntt_supports(K)) return fail(WM_EUNSUPPORTED, "limb count not built into the NTT kernels");
+  if (f->mont && !mont_supports(K))
+    return fail(WM_EUNSUPPORTED, "limb count not built into the full-width NTT kernels");
   // Shoup needs p < 2^(32K-2): guaranteed by the field's p < 2^(32K-4).
   wm_ntt_plan *pl = new wm_ntt_plan();
   pl->field = f;
@@ -822,6 +925,7 @@ int wm_ntt_plan_create(const wm_field *f, int64_t n, const uint32_t *root_host, 
   pl->logn = 63 - __builtin_clzll((unsigned long long)n);
   Big root(root_host, root_host + K), root_inv(root_inv_host, root_inv_host + K);
   pl->ninv = Big(n_inv_host, n_inv_host + K);
+  if (f->mont) pl->ninv_mont = to_mont(pl->ninv, f->q);
   // Shoup companion of n^-1 and np = 2^(32K) - p on the host.
   {
     Big num = big_shl(pl->ninv, 32 * K, 2 * K);
@@ -992,7 +1096,15 @@ int wm_ntt_twiddles(const wm_ntt_plan *p, int inverse, int64_t count, uint32_t *
   switch (p->K) {
 #define WM_CASE(k)                                                                             \
   case k:                                                                                      \
-    twiddle_extract_kernel<k><<<grid, 256, 0, (cudaStream_t)stream>>>(table, count, out);      \
+    if constexpr (mont_ntt_built<k>()) {                                                       \
+      if (p->field->mont) {                                                                    \
+        twiddle_extract_kernel<k, true><<<grid, 256, 0, (cudaStream_t)stream>>>(              \
+            table, count, out, field_const<k>(p->field));                                      \
+        break;                                                                                 \
+      }                                                                                        \
+    }                                                                                          \
+    twiddle_extract_kernel<k, false><<<grid, 256, 0, (cudaStream_t)stream>>>(                 \
+        table, count, out, field_const<k>(p->field));                                          \
     break;
     WM_NTT_KS(WM_CASE)
 #undef WM_CASE

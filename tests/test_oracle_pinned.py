@@ -186,3 +186,20 @@ def test_ntt_points_matches_transform():
     ks = [0, 1, 7, 511, 1023]
     pts = f.ntt_points(x, prm["root"], ks)
     assert ints(pts) == [ints(y[k:k + 1])[0] for k in ks]
+
+
+def test_exact_ntt_restatement_matches_reference_executor():
+    """run_ntt_exact (general-modulus restatement, for full-width fields)
+    equals the reference-faithful run_ntt where both apply, and ntt_point
+    equals the O(n^2) ntt_reference at single indices."""
+    assert bigint.run_ntt_exact([1, 2, 3, 4], 13, 5, 10) == [10, 1, 11, 8]  # test_kernels.py:161
+    for width, n in [(16, 16), (64, 64), (256, 128)]:
+        prm = bigint.find_ntt_params(width, n)
+        rng = np.random.Generator(np.random.PCG64(width))
+        x = bigint.uniform_residues(rng, n, prm["p"])
+        assert bigint.run_ntt_exact(x, prm["p"], prm["root"], prm["n_inv"]) == bigint.run_ntt(x, prm, width)
+        y = bigint.run_ntt(x, prm, width)
+        assert bigint.run_ntt_exact(y, prm["p"], prm["root_inv"], prm["n_inv"], inverse=True) == x
+        ref = bigint.ntt_reference(x, prm["p"], prm["root"], prm["root_inv"], prm["n_inv"])
+        for k in (0, 1, n - 1, n // 3):
+            assert bigint.ntt_point(x, prm["p"], prm["root"], k) == ref[k]
