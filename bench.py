@@ -195,6 +195,7 @@ def run_gpu(args, rank, world, local, pg):
         plan.forward(x, out=y, workspace=ws)
         plan.inverse(y, out=z, workspace=ws)
 
+    bufs = e2e_host_buffers(torch, field)
     launches_per_step = 2 * len(plan.pass_log_sizes)
 
     for _ in range(args.warmup):
@@ -232,7 +233,7 @@ def run_gpu(args, rank, world, local, pg):
     pass0_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
 
     # ---- end-to-end through the C ABI with host buffers (reference layout)
-    e2e = run_e2e(args, torch, dev, plan, field, ws, pg, world)
+    e2e = run_e2e(args, torch, plan, bufs, pg, world)
 
     # ---- extras: BLAS sweep (configs[2]), four-step single 2^24 NTT (configs[4]), reference GPU code
     blas = run_blas(args, torch, field, pg) if not args.skip_extras else None
@@ -257,15 +258,25 @@ def run_gpu(args, rank, world, local, pg):
     }
 
 
-def run_e2e(args, torch, dev, plan, field, ws, pg, world):
-    """Public API end to end: pinned HOST buffers in the reference layout
-    (AoS, 4 x 64-bit words MSW first per 256-bit value, kernels.to_words)
-    through the pipelined C ABI call wm_ntt_host (chunked H2D / layout
-    convert + NTT + INTT + convert / D2H on overlapping streams)."""
+def e2e_host_buffers(torch, field):
+    """Pinned host buffers of one step in the reference layout (AoS, 4 x
+    64-bit words MSW first per 256-bit value, kernels.to_words).  Allocated
+    before the device-resident timing: on the VM hosts of this pool, pinned
+    buffers allocated after it ran ~20 % slower over PCIe for the whole
+    measurement (tools/e2e_bisect.py)."""
     host_in = torch.empty((BATCH * N, WORDS64), dtype=torch.int64, pin_memory=True)
     host_out = torch.empty((BATCH * N, WORDS64), dtype=torch.int64, pin_memory=True)
     src = canonical_random(torch, BATCH * N, 99)
     host_in.copy_(field.to_ref_layout(src, 64, WORDS64).cpu())
+    host_out.zero_()
+    return host_in, host_out
+
+
+def run_e2e(args, torch, plan, bufs, pg, world):
+    """Public API end to end: pinned HOST buffers in the reference layout
+    through the pipelined C ABI call wm_ntt_host (chunked H2D / layout
+    convert + NTT + INTT + convert / D2H on overlapping streams)."""
+    host_in, host_out = bufs
     stream = torch.cuda.current_stream()
 
     def step():

@@ -15,6 +15,7 @@
 // kComp compute streams and the kernels of consecutive chunks run
 // concurrently; the copies, not the kernels, then bound the pipeline.
 #include <algorithm>
+#include <vector>
 
 #include "wm_internal.cuh"
 
@@ -82,8 +83,28 @@ extern "C" int wm_ntt_host(const wm_ntt_plan *pc, int mode, int word_bits, int r
   wm_ntt_plan *p = const_cast<wm_ntt_plan *>(pc);
   const int64_t n = p->n;
   const int K = p->K;
-  if (chunk == 0) chunk = std::max<int64_t>(1, (int64_t)(4 << 20) / (n * K * 4));  // ~4 MiB of limbs (tools/e2e_sweep.sh)
+  // Chunk schedule.  auto (chunk == 0): ~8 MiB of limbs per chunk (PCIe runs
+  // at ~90 GB/s both ways from 4 MiB chunks up, profiles/r01_pcie_chunks.txt),
+  // with the chunks at both ends halved down to one transform so the
+  // pipeline's fill (first H2D alone) and drain (last kernels + D2H alone)
+  // cost a fraction of a full chunk.  An explicit chunk size is used as given.
+  std::vector<int64_t> sizes;
+  if (chunk == 0) {
+    chunk = std::min<int64_t>(batch, std::max<int64_t>(1, (int64_t)(8 << 20) / (n * K * 4)));
+    std::vector<int64_t> ramp;
+    for (int64_t r = 1; r < chunk; r *= 2) ramp.push_back(r);
+    int64_t ramp_total = 0;
+    for (int64_t r : ramp) ramp_total += 2 * r;
+    if (batch >= ramp_total + chunk) {
+      int64_t mid = batch - ramp_total;
+      sizes = ramp;
+      for (; mid > 0; mid -= chunk) sizes.push_back(std::min(chunk, mid));
+      for (auto it = ramp.rbegin(); it != ramp.rend(); ++it) sizes.push_back(*it);
+    }
+  }
   chunk = std::min(chunk, batch);
+  if (sizes.empty())
+    for (int64_t t = 0; t < batch; t += chunk) sizes.push_back(std::min(chunk, batch - t));
   const size_t ref_bytes_per_t = (size_t)n * ref_words * (word_bits / 8);
   const size_t limb_bytes_per_t = (size_t)n * K * 4;
   const size_t ref_sz = align256(ref_bytes_per_t * chunk);
@@ -99,12 +120,14 @@ extern "C" int wm_ntt_host(const wm_ntt_plan *pc, int mode, int word_bits, int r
   WM_CUDA_TRY(cudaEventRecord(p->ev_entry, user));
   for (int i = 0; i < wm_ntt_plan::kStreams; ++i) WM_CUDA_TRY(cudaStreamWaitEvent(p->hs[i], p->ev_entry, 0));
 
-  const int64_t nchunks = (batch + chunk - 1) / chunk;
+  const int64_t nchunks = (int64_t)sizes.size();
+  int64_t t_next = 0;
   for (int64_t c = 0; c < nchunks; ++c) {
     const int s = (int)(c % wm_ntt_plan::kSlots);
     cudaStream_t comp = p->hs[2 + c % wm_ntt_plan::kComp];
-    const int64_t t0 = c * chunk;
-    const int64_t nt = std::min(chunk, batch - t0);
+    const int64_t t0 = t_next;
+    const int64_t nt = sizes[c];
+    t_next += nt;
     char *base = static_cast<char *>(p->slot_mem[s]);
     void *d_ref = base;
     uint32_t *d_a = reinterpret_cast<uint32_t *>(base + ref_sz);
