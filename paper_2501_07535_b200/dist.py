@@ -141,7 +141,18 @@ class SymmComm:
         self.group = group if group is not None else dist.group.WORLD
         self.rank = dist.get_rank(self.group)
         self.world = dist.get_world_size(self.group)
-        self.recv = symm.empty(n_words, dtype=torch.int32, device=torch.device("cuda", torch.cuda.current_device()))
+        dev = torch.device("cuda", torch.cuda.current_device())
+        # the local allocation can fail on one rank only; agree before the
+        # collective rendezvous so no rank is left waiting in it
+        err = None
+        try:
+            self.recv = symm.empty(n_words, dtype=torch.int32, device=dev)
+        except Exception as exc:  # noqa: BLE001 - reported after the agreement
+            err = exc
+        ok = torch.tensor([0 if err is None else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MAX, group=self.group)
+        if int(ok.item()):
+            raise RuntimeError(f"symmetric memory allocation failed on some rank: {err}")
         self.handle = symm.rendezvous(self.recv, self.group.group_name)
         self.peer_ptrs = [int(p) for p in self.handle.buffer_ptrs]
         if len(self.peer_ptrs) != self.world:
