@@ -175,7 +175,11 @@ __global__ void __launch_bounds__(256) blas_kernel(const uint32_t *a, const uint
       } else if constexpr (OP == OP_VSUB) {
         sub_mod<K>(r, x, y, args.F.q);
       } else if constexpr (OP == OP_VMUL) {
-        mul_mont_plain<K>(r, x, y, args.F);
+        if (args.F.s <= 31) {
+          mul_barrett_full<K>(r, x, y, args.F);
+        } else {
+          mul_mont_plain<K>(r, x, y, args.F);
+        }
       } else {  // scal = a R mod q: one Montgomery product gives a x
         uint32_t t[K];
         mont_mul<K>(t, args.scal, x, args.F.q, args.F.qinv);
@@ -364,13 +368,28 @@ int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags,
     f->mont = true;
     f->bits = bits;
     f->K = K;
-    f->s = 0;
     f->q = q;
     Big zero(K, 0u);
     f->qn = q;
     f->qn2 = zero;
     f->nqn = zero;
     f->mu8 = zero;
+    // full-width Barrett constants for vmul (mul_barrett_full) when the
+    // modulus fills the top limb: qn = q << s (top bit set), mu_lo = low K
+    // limbs of floor(2^(64K) / qn) = 2^(32K) + mu_lo; else s = 32 marks
+    // "no Barrett" and vmul takes two Montgomery products
+    f->s = 32 * K - qb;
+    if (f->s <= 31) {
+      f->qn = big_shl(q, f->s, K);
+      Big mu = big_pow2_div(64 * K, f->qn, K + 1);
+      if (mu[K] != 1u) {
+        delete f;
+        return fail(WM_EINVAL, "internal: full-width Barrett constant out of range");
+      }
+      f->mu8 = big_resize(mu, K);
+    } else {
+      f->s = 32;
+    }
     uint32_t x = q[0];  // Newton: inverse of q mod 2^32 (x = q is correct mod 8)
     for (int i = 0; i < 4; ++i) x *= 2u - q[0] * x;
     f->qinv = 0u - x;

@@ -643,6 +643,90 @@ WM_DEV void mont_mul(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&
   select_n<K>(r, t[K] | (br ^ 0xffffffffu), d, lo);
 }
 
+// a b mod q for a full-width field by Barrett reduction (one product chain
+// instead of two Montgomery products).  The modulus is normalised to
+// qn = q << s with its top bit at 2^(M-1), M = 32K; mu = floor(2^(2M)/qn) =
+// 2^M + mu_lo has an implicit leading one.  With t = (a << s) b:
+//   q1 = t >> (M-1)                       (K+1 limbs, top limb <= 1)
+//   X  = q1 mu_lo >> M                    (truncated high half, + q1_top mu_lo)
+//   q3 = (q1 + X) >> 1                    (within 4 of floor(t / qn))
+//   r  = t - q3 qn  mod 2^(32(K+1))       (< 5 qn: three conditional
+//                                          subtractions of 4qn, 2qn, qn)
+// and the result is r >> s.  F.qn = qn, F.mu8 = mu_lo, F.s = s for these
+// fields.  ~K^2 + K^2/2 + K(K+1)/2 + K word products.
+template <int K>
+WM_DEV void mul_barrett_full(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K],
+                             const FieldConst<K> &F) {
+  uint32_t as[K];
+  shl_small<K>(as, a, F.s);
+  uint32_t t[2 * K];
+  mul_full<K, kU64>(t, as, b);
+  // q1 = t >> (32K - 1)
+  uint32_t q1[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) q1[j] = __funnelshift_r(t[K - 1 + j], t[K + j], 31);
+  const uint32_t q1top = t[2 * K - 1] >> 31;
+  // X = hi(q1_lo mu_lo) + q1top * mu_lo   (K+1 limbs)
+  uint32_t x[K + 1];
+  {
+    uint32_t h[K], m[K];
+    mul_hi_trunc<K, kU64>(h, q1, F.mu8);
+#pragma unroll
+    for (int j = 0; j < K; ++j) m[j] = q1top ? F.mu8[j] : 0u;
+    const uint32_t c = add_n<K>(h, h, m);
+#pragma unroll
+    for (int j = 0; j < K; ++j) x[j] = h[j];
+    x[K] = c;
+  }
+  // y = q1 + X (K+1 limbs), q3 = y >> 1
+  uint32_t y[K + 1], q1w[K + 1];
+#pragma unroll
+  for (int j = 0; j < K; ++j) q1w[j] = q1[j];
+  q1w[K] = q1top;
+  add_n<K + 1>(y, q1w, x);
+  uint32_t q3[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) q3[j] = __funnelshift_r(y[j], y[j + 1], 1);
+  const uint32_t q3top = y[K] >> 1;
+  // r = t - q3 qn  (low K+1 limbs)
+  uint32_t pq[K + 1];
+#pragma unroll
+  for (int j = 0; j <= K; ++j) pq[j] = 0u;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {  // rows of q3_lo * qn reaching limbs i..K
+    uint32_t c = 0;
+#pragma unroll
+    for (int j = 0; j + i < K; ++j) {
+      const uint64_t p = (uint64_t)F.qn[j] * q3[i] + pq[i + j] + c;
+      pq[i + j] = (uint32_t)p;
+      c = (uint32_t)(p >> 32);
+    }
+    if (i > 0) pq[K] += F.qn[K - i] * q3[i];  // top column: low halves only
+    pq[K] += c;
+  }
+  pq[K] += q3top * F.qn[0];
+  uint32_t tl[K + 1], rr[K + 1];
+#pragma unroll
+  for (int j = 0; j <= K; ++j) tl[j] = t[j];
+  sub_n<K + 1>(rr, tl, pq);
+  // r < 5 qn < 2^(32K+3): subtract 4qn, 2qn, qn where they fit
+  uint32_t m[K + 1];
+#pragma unroll
+  for (int sh = 2; sh >= 0; --sh) {
+#pragma unroll
+    for (int j = 0; j <= K; ++j) {
+      const uint32_t lo = j < K ? F.qn[j] : 0u;
+      const uint32_t below = j > 0 ? F.qn[j - 1] : 0u;
+      m[j] = sh ? __funnelshift_l(below, lo, sh) : lo;
+    }
+    cond_sub<K + 1>(rr, m);
+  }
+  uint32_t lo[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) lo[j] = __funnelshift_r(rr[j], rr[j + 1], F.s);
+  copy_n<K>(r, lo);
+}
+
 // a b mod q for a Montgomery field: two Montgomery products (a b R^-1, then
 // times R^2 R^-1).
 template <int K>

@@ -23,6 +23,8 @@ CASES = [
     (256, SECP256K1_P), (256, BLS12_381_R), (256, BN254_P), (384, BLS12_381_P),
     (64, GOLDILOCKS), (128, M127), (32, 2**32 - 5), (1024, 2**1024 - 1),
     (768, 2**768 - 1), (512, 2**512 - 569),
+    # moduli that leave the top limb empty (vmul takes the two-Montgomery-product path)
+    (256, M127), (1024, SECP256K1_P), (64, 2**32 - 5),
 ]
 
 
