@@ -40,7 +40,11 @@
 #ifndef WM_NTT_MINB_SMALL  // K <= 4 (<= 128-bit): lighter register footprint
 #define WM_NTT_MINB_SMALL 2
 #endif
-#define WM_NTT_BOUNDS(K) __launch_bounds__(256, ((K) <= 4 ? WM_NTT_MINB_SMALL : (K) <= 12 ? WM_NTT_MINB : 1))
+#ifndef WM_NTT_MINB_WIDE  // K > 12: 2 CTAs/SM with a few spilled registers beat
+#define WM_NTT_MINB_WIDE 2   // 1 CTA/SM (profiles/r01_ab_wide_occupancy.txt: 768-bit 102 -> 91 us)
+#endif
+#define WM_NTT_BOUNDS(K) \
+  __launch_bounds__(256, ((K) <= 4 ? WM_NTT_MINB_SMALL : (K) <= 12 ? WM_NTT_MINB : WM_NTT_MINB_WIDE))
 // Target tile size (32-bit words of data per CTA; 16384 = 64 KB).
 #ifndef WM_NTT_TILE_WORDS
 #define WM_NTT_TILE_WORDS 16384
