@@ -808,9 +808,15 @@ def main():
     bflies = BATCH * (N // 2) * sizes[0]  # one pass = log2(L) radix-2 stages over the batch
     achieved = bflies * ALG_WMUL_PER_BFLY / (pass_ms * 1e-3)
     traffic = None
+    pipes = None
     try:
         prof = json.loads((ROOT / "profiles" / "r01_ncu_traffic.json").read_text())
-        traffic = prof["ntt_col_pass<8>"]["dram_bytes_per_launch"]
+        kp = prof.get("ntt_col_pass<8, 0>") or prof["ntt_col_pass<8>"]
+        traffic = kp["dram_bytes_per_launch"]
+        pipes = {"fmaheavy_pct": kp.get("fmaheavy_pct"), "alu_pct": kp.get("alu_pct"),
+                 "basis": "ncu --set full of the same kernel (profiles/r01_ncu_traffic.json): the "
+                          "IMAD/IMAD.WIDE (FMA-heavy) pipe is the binding unit; the kernels execute ~0.5 "
+                          "of the reference's 3k^2 products per butterfly (Shoup + lazy reduction)"}
     except Exception:
         pass
     roofline = {
@@ -824,6 +830,7 @@ def main():
         "traffic_basis": "dram__bytes_read+write per launch, ncu --set full (profiles/r01_ncu_traffic.json); "
                          "algorithmic bytes per launch = 2 x 128 MiB",
         "ns_per_butterfly_paper_metric": 2 * (res["ms_per_step"] * 1e6 / (2 * BATCH)) / (N * LOGN),
+        "pipe_utilisation": pipes,
     }
     cpu = None
     if world == 1:
