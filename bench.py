@@ -822,7 +822,7 @@ def main():
     roofline = {
         "bound": "int", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Twmul/s",
         "frac": achieved / peak, "traffic": traffic,
-        "kernel": f"ntt_col_pass<8> (pass 0 of {'+'.join('2^%d' % s for s in sizes)}), batch 64, {pass_ms * 1e3:.1f} us/launch",
+        "kernel": f"ntt_col_pass<8, 0> (pass 0 of {'+'.join('2^%d' % s for s in sizes)}), batch 64, {pass_ms * 1e3:.1f} us/launch",
         "work": f"{ALG_WMUL_PER_BFLY} word products per butterfly (reference 3k^2, SURVEY.md \u00a78(d)) x "
                 f"batch*(n/2)*log2(L) butterflies per launch = {bflies * ALG_WMUL_PER_BFLY:.4g}",
         "peak_basis": f"32 IMAD.WIDE/clk/SM x 148 SMs x {clk:.0f} MHz (half-rate IMAD.WIDE measured, "
