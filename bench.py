@@ -185,6 +185,15 @@ def run_gpu(args, rank, world, local, pg):
     field = plan.field
     stream = torch.cuda.current_stream()
 
+    # e2e host buffer and one e2e call before the large device buffers:
+    # wm_ntt_host creates its streams and device staging slots on first use,
+    # and slots allocated after ~1 GB of other device buffers made every later
+    # e2e step ~10 % slower on this pool (tools/e2e_bisect.py)
+    bufs = e2e_host_buffers(torch, field)
+    plan.host_transform(bufs[0], bufs[1], mode="forward_inverse", word_bits=64, ref_words=WORDS64,
+                        chunk=args.e2e_chunk)
+    torch.cuda.synchronize()
+
     x = canonical_random(torch, BATCH * N, 1234 + rank)
     y = torch.empty_like(x)
     z = torch.empty_like(x)
@@ -195,7 +204,6 @@ def run_gpu(args, rank, world, local, pg):
         plan.forward(x, out=y, workspace=ws)
         plan.inverse(y, out=z, workspace=ws)
 
-    bufs = e2e_host_buffers(torch, field)
     launches_per_step = 2 * len(plan.pass_log_sizes)
 
     for _ in range(args.warmup):
@@ -259,17 +267,16 @@ def run_gpu(args, rank, world, local, pg):
 
 
 def e2e_host_buffers(torch, field):
-    """Pinned host buffers of one step in the reference layout (AoS, 4 x
-    64-bit words MSW first per 256-bit value, kernels.to_words).  Allocated
-    before the device-resident timing: on the VM hosts of this pool, pinned
-    buffers allocated after it ran ~20 % slower over PCIe for the whole
-    measurement (tools/e2e_bisect.py)."""
-    host_in = torch.empty((BATCH * N, WORDS64), dtype=torch.int64, pin_memory=True)
-    host_out = torch.empty((BATCH * N, WORDS64), dtype=torch.int64, pin_memory=True)
+    """The step's pinned host buffer in the reference layout (AoS, 4 x 64-bit
+    words MSW first per 256-bit value, kernels.to_words), transformed in place
+    (wm_ntt_host reads chunk c before it writes chunk c back).  One buffer
+    instead of an input and an output buffer: on the VM hosts of this pool a
+    larger pinned footprint made PCIe transfers 5-30 % slower and erratic
+    (tools/e2e_inplace.py, profiles/r01_e2e_ab.txt).  Allocated before the
+    device-resident timing for the same reason."""
     src = canonical_random(torch, BATCH * N, 99)
-    host_in.copy_(field.to_ref_layout(src, 64, WORDS64).cpu())
-    host_out.zero_()
-    return host_in, host_out
+    host = field.to_ref_layout(src, 64, WORDS64).cpu().pin_memory()
+    return host, host
 
 
 def run_e2e(args, torch, plan, bufs, pg, world):
@@ -283,10 +290,12 @@ def run_e2e(args, torch, plan, bufs, pg, world):
         plan.host_transform(host_in, host_out, mode="forward_inverse", word_bits=64, ref_words=WORDS64,
                             chunk=args.e2e_chunk)
 
+    want = host_in.clone()
     for _ in range(max(1, args.warmup)):
         step()
     torch.cuda.synchronize()
-    assert torch.equal(host_out, host_in), "e2e roundtrip mismatch"
+    assert torch.equal(host_out, want), "e2e roundtrip mismatch"
+    del want
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier(pg)
     torch.cuda.synchronize()
@@ -327,8 +336,8 @@ def run_e2e(args, torch, plan, bufs, pg, world):
             "pcie_floor_basis": "the step's H2D and D2H bytes as two concurrent whole-buffer copies "
                                 "(pinned host <-> device, no kernels), same unit",
             "h2d_bytes_per_step": nbytes, "d2h_bytes_per_step": nbytes,
-            "path": "NttPlan.host_transform -> C ABI wm_ntt_host(mode=FWD_INV): pinned host buffers, "
-                    "reference layout, chunked H2D/compute/D2H pipeline",
+            "path": "NttPlan.host_transform -> C ABI wm_ntt_host(mode=FWD_INV): pinned host buffer "
+                    "(reference layout) transformed in place, chunked H2D/compute/D2H pipeline",
             "chunk_transforms": args.e2e_chunk or "auto"}
 
 
