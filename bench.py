@@ -752,7 +752,7 @@ def reference_arm(args, rank, world, pg):
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": wall * 1e3 / args.steps, "higher_is_better": False, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32 limbs (256-bit integers)", "data": "synthetic",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": "256-bit forward+inverse NTT n=2^16 (sample of the batch-64 step)",
                    "bits": BITS, "n": N, "transforms_per_step": 2 * (per_step // 2)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
@@ -858,7 +858,7 @@ def main():
         "higher_is_better": False,
         "scaling": "weak",
         "vs_baseline": None,
-        "dtype": "u32 limbs (256-bit integers)",
+        "dtype": "u32",
         "data": "synthetic",
         "config": {"workload": "256-bit forward+inverse NTT n=2^16 batch 64 per GPU (BASELINE configs[1])",
                    "bits": BITS, "n": N, "batch_per_gpu": BATCH, "transforms_per_step": 2 * BATCH,
