@@ -249,6 +249,7 @@ def run_gpu(args, rank, world, local, pg):
     b20 = run_batched_2p20(args, torch, rank, world, pg) if not args.skip_extras else None
     refgpu = run_reference_gpu(args, torch, plan) if (world == 1 and not args.skip_extras) else None
     fullw = run_full_width(args, torch) if not args.skip_extras else None
+    steady = run_steady_state(args, torch, plan) if not args.skip_extras else None
 
     return {
         "us_per_transform": us_per_transform,
@@ -263,6 +264,7 @@ def run_gpu(args, rank, world, local, pg):
         "batched_2p20": b20,
         "reference_gpu": refgpu,
         "full_width": fullw,
+        "steady_state": steady,
     }
 
 
@@ -537,6 +539,37 @@ def run_full_width(args, torch):
     del a, b, o
     torch.cuda.empty_cache()
     return res
+
+
+def run_steady_state(args, torch, plan):
+    """The paper's protocol: t_single = t_all / k at
+    several batch sizes k, and ns per butterfly = 2 t_single / (n log2 n);
+    256-bit n = 2^16 forward + inverse, device-resident."""
+    stream = torch.cuda.current_stream()
+    rows = []
+    for k in (8, 32, 64, 128, 256):
+        x = canonical_random(torch, k * N, 31 + k)
+        y, z = torch.empty_like(x), torch.empty_like(x)
+        ws = torch.empty(plan.workspace_bytes(k) // 4, dtype=torch.int32, device="cuda")
+        for _ in range(2):
+            plan.forward(x, out=y, workspace=ws)
+            plan.inverse(y, out=z, workspace=ws)
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(5)]
+        for e0, e1 in evs:
+            e0.record(stream)
+            plan.forward(x, out=y, workspace=ws)
+            plan.inverse(y, out=z, workspace=ws)
+            e1.record(stream)
+        torch.cuda.synchronize()
+        ms = statistics.median(a.elapsed_time(b) for a, b in evs)
+        t_single = ms * 1e3 / (2 * k)
+        rows.append({"batch": k, "us_per_transform": round(t_single, 3),
+                     "ns_per_butterfly": round(2 * t_single * 1e3 / (N * LOGN), 5)})
+        del x, y, z, ws
+    torch.cuda.empty_cache()
+    return {"rows": rows, "t_single_us": min(r["us_per_transform"] for r in rows),
+            "note": "median of 5; inputs of 8 transforms and up fit in L2 partially (not flushed)"}
 
 
 def run_batched_2p20(args, torch, rank, world, pg):
@@ -874,6 +907,7 @@ def main():
         "batched_2p20_x256": res["batched_2p20"],
         "reference_gpu": res["reference_gpu"],
         "full_width_bls12_381": res["full_width"],
+        "steady_state_2p16": res["steady_state"],
     }
     emit(out)
     if pg is not None:
