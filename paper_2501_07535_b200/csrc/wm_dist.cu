@@ -89,7 +89,7 @@ struct ScatterDst {
 // transposed tile rows are stored straight into the destination ranks'
 // receive buffers (the four-step all-to-all fused into the producing kernel:
 // each 32-element row segment is one coalesced remote store burst).
-template <int K>
+template <int K, bool MONT>
 __global__ void __launch_bounds__(256) scale_transpose_kernel(const uint32_t *in, const uint32_t *table,
                                                               uint32_t *out, int64_t rows, int64_t cols,
                                                               const __grid_constant__ FieldConst<K> F,
@@ -114,7 +114,11 @@ __global__ void __launch_bounds__(256) scale_transpose_kernel(const uint32_t *in
       ldg_elem<K>(v, in + (r * cols + c) * K);
       ldg_elem<K>(w, table + (r * cols + c) * (2 * K));
       ldg_elem<K>(wp, table + (r * cols + c) * (2 * K) + K);
-      mul_shoup<K>(res, v, w, wp, p, np);
+      if constexpr (MONT) {  // full-width field: table holds w R mod p
+        mont_mul<K>(res, v, w, p, F.qinv);
+      } else {
+        mul_shoup<K>(res, v, w, wp, p, np);
+      }
 #pragma unroll
       for (int j = 0; j < K; ++j) tile[rr * stride + cc * K + j] = res[j];
     }
@@ -137,12 +141,26 @@ __global__ void __launch_bounds__(256) scale_transpose_kernel(const uint32_t *in
   }
 }
 
-// table[r][c] = (root^((row0 + r) * c mod n), companion), one thread per
-// chunk of a row: exponentiate once, then step by root^(row0 + r).
+template <int K, bool MONT>
+WM_DEV void dist_mul(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K], const FieldConst<K> &F) {
+  if constexpr (MONT) mont_mul<K>(r, a, b, F.q, F.qinv); else mul_barrett<K>(r, a, b, F);
+}
+
+// Limb counts with a full-width (Montgomery) instantiation of these kernels.
 template <int K>
+constexpr bool dist_mont_built() {
+#define WM_EQ(k) || K == k
+  return false WM_MONT_KS(WM_EQ);
+#undef WM_EQ
+}
+
+// table[r][c] = (root^((row0 + r) * c mod n), companion), one thread per
+// chunk of a row: exponentiate once, then step by root^(row0 + r).  MONT: the
+// root and `one` arrive in Montgomery form, the table holds root^e R mod p.
+template <int K, bool MONT>
 __global__ void twiddle_2d_kernel(uint32_t *table, int64_t n, int64_t row0, int64_t rows, int64_t cols,
                                   int64_t chunk, const __grid_constant__ FieldConst<K> F,
-                                  const __grid_constant__ Limbs<K> root) {
+                                  const __grid_constant__ Limbs<K> root, const __grid_constant__ Limbs<K> one) {
   const int64_t per_row = (cols + chunk - 1) / chunk;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= rows * per_row) return;
@@ -152,14 +170,13 @@ __global__ void twiddle_2d_kernel(uint32_t *table, int64_t n, int64_t row0, int6
   auto powmod = [&](uint32_t (&out)[K], uint64_t e) {
     uint32_t b[K], tmp[K];
     copy_n<K>(b, root.v);
-    zero_n<K>(out);
-    out[0] = 1;
+    copy_n<K>(out, one.v);
     for (; e; e >>= 1) {
       if (e & 1) {
-        mul_barrett<K>(tmp, out, b, F);
+        dist_mul<K, MONT>(tmp, out, b, F);
         copy_n<K>(out, tmp);
       }
-      mul_barrett<K>(tmp, b, b, F);
+      dist_mul<K, MONT>(tmp, b, b, F);
       copy_n<K>(b, tmp);
     }
   };
@@ -168,40 +185,67 @@ __global__ void twiddle_2d_kernel(uint32_t *table, int64_t n, int64_t row0, int6
   powmod(step, j1 & (uint64_t)(n - 1));
   for (int64_t c = c0; c < c1; ++c) {
     uint32_t wp[K], tmp[K];
-    shoup_companion_dev<K>(wp, x, F.q);
+    if constexpr (MONT) zero_n<K>(wp); else shoup_companion_dev<K>(wp, x, F.q);
     stg_elem<K>(table + (r * cols + c) * (2 * K), x);
     stg_elem<K>(table + (r * cols + c) * (2 * K) + K, wp);
-    mul_barrett<K>(tmp, x, step, F);
+    dist_mul<K, MONT>(tmp, x, step, F);
     copy_n<K>(x, tmp);
   }
 }
 
 
-template <int K>
-static int launch_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out,
-                                  int64_t rows, int64_t cols, cudaStream_t st, const ScatterDst &D) {
+template <int K, bool MONT>
+static int launch_scale_transpose_t(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out,
+                                    int64_t rows, int64_t cols, cudaStream_t st, const ScatterDst &D) {
   const size_t smem = (size_t)TT * (TT * K + 1) * 4;
   static bool attr = false;
   if (!attr) {
-    WM_CUDA_TRY(cudaFuncSetAttribute(scale_transpose_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    WM_CUDA_TRY(cudaFuncSetAttribute(scale_transpose_kernel<K, MONT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<size_t>(smem, 48 * 1024)));
     attr = true;
   }
   dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)((rows + TT - 1) / TT));
-  scale_transpose_kernel<K><<<grid, 256, smem, st>>>(in, table, out, rows, cols, field_const<K>(f), D);
+  scale_transpose_kernel<K, MONT><<<grid, 256, smem, st>>>(in, table, out, rows, cols, field_const<K>(f), D);
   WM_LAUNCH_CHECK("scale_transpose launch");
   return WM_OK;
 }
 
 template <int K>
+static int launch_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out,
+                                  int64_t rows, int64_t cols, cudaStream_t st, const ScatterDst &D) {
+  if constexpr (dist_mont_built<K>()) {
+    if (f->mont) return launch_scale_transpose_t<K, true>(f, in, table, out, rows, cols, st, D);
+  }
+  if (f->mont) return fail(WM_EUNSUPPORTED, "limb count not built into the full-width kernels");
+  return launch_scale_transpose_t<K, false>(f, in, table, out, rows, cols, st, D);
+}
+
+template <int K>
 static int launch_twiddle_2d(const wm_field *f, int64_t n, const uint32_t *root, int64_t row0, int64_t rows,
                              int64_t cols, uint32_t *table, cudaStream_t st) {
-  Limbs<K> rt;
-  for (int j = 0; j < K; ++j) rt.v[j] = root[j];
+  Big r(root, root + K), one(K, 0u);
+  one[0] = 1;
+  if (f->mont) {
+    r = to_mont(r, f->q);
+    one = to_mont(one, f->q);
+  }
+  Limbs<K> rt, on;
+  for (int j = 0; j < K; ++j) {
+    rt.v[j] = r[j];
+    on.v[j] = one[j];
+  }
   const int64_t chunk = 64;
   const int64_t threads = rows * ((cols + chunk - 1) / chunk);
   const int grid = (int)((threads + 127) / 128);
-  twiddle_2d_kernel<K><<<grid, 128, 0, st>>>(table, n, row0, rows, cols, chunk, field_const<K>(f), rt);
+  if constexpr (dist_mont_built<K>()) {
+    if (f->mont) {
+      twiddle_2d_kernel<K, true><<<grid, 128, 0, st>>>(table, n, row0, rows, cols, chunk, field_const<K>(f), rt, on);
+      WM_LAUNCH_CHECK("twiddle_2d launch");
+      return WM_OK;
+    }
+  }
+  if (f->mont) return fail(WM_EUNSUPPORTED, "limb count not built into the full-width kernels");
+  twiddle_2d_kernel<K, false><<<grid, 128, 0, st>>>(table, n, row0, rows, cols, chunk, field_const<K>(f), rt, on);
   WM_LAUNCH_CHECK("twiddle_2d launch");
   return WM_OK;
 }
@@ -239,7 +283,6 @@ int wm_transpose(int words, const uint32_t *in, uint32_t *out, int64_t rows, int
 
 int wm_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out, int64_t rows,
                        int64_t cols, void *stream) {
-  if (f && f->mont) return fail(WM_EUNSUPPORTED, "the distributed four-step supports reference-range (Barrett) fields only");
   if (!f) return fail(WM_EINVAL, "null field");
   if (rows < 0 || cols < 0) return fail(WM_EINVAL, "bad shape");
   if (rows == 0 || cols == 0) return WM_OK;
@@ -260,7 +303,6 @@ int wm_scale_transpose(const wm_field *f, const uint32_t *in, const uint32_t *ta
 int wm_scale_transpose_scatter(const wm_field *f, const uint32_t *in, const uint32_t *table,
                                const uint64_t *dst_ptrs, int P, int src_rank, int64_t rows, int64_t cols,
                                void *stream) {
-  if (f && f->mont) return fail(WM_EUNSUPPORTED, "the distributed four-step supports reference-range (Barrett) fields only");
   if (!f) return fail(WM_EINVAL, "null field");
   if (rows < 0 || cols < 0) return fail(WM_EINVAL, "bad shape");
   if (P < 1 || P > kMaxPeers) return fail(WM_EUNSUPPORTED, "peer count outside 1..16");
@@ -291,7 +333,6 @@ int wm_scale_transpose_scatter(const wm_field *f, const uint32_t *in, const uint
 
 int wm_twiddle_table_2d(const wm_field *f, int64_t n, const uint32_t *root_host, int64_t row0, int64_t rows,
                         int64_t cols, uint32_t *table, void *stream) {
-  if (f && f->mont) return fail(WM_EUNSUPPORTED, "the distributed four-step supports reference-range (Barrett) fields only");
   if (!f || !root_host || !table) return fail(WM_EINVAL, "null argument");
   if (n < 1 || (n & (n - 1)) || rows < 0 || cols < 0 || row0 < 0) return fail(WM_EINVAL, "bad shape");
   if (rows == 0 || cols == 0) return WM_OK;

@@ -165,7 +165,8 @@ class SymmComm:
 class DeviceBackend:
     """Rank-local compute on the B200 (C ABI kernels)."""
 
-    def __init__(self, bits: int, params: NttParams, layout: FourStepLayout, rank: int):
+    def __init__(self, bits: int, params: NttParams, layout: FourStepLayout, rank: int,
+                 strategy: str = "schoolbook"):
         import torch
 
         from .device import Field, NttPlan, ints_to_limbs
@@ -175,7 +176,7 @@ class DeviceBackend:
         p, n = params.p, params.n
         w, wi = params.root, params.root_inv
         n1, n2, P = layout.n1, layout.n2, layout.world
-        self.field = Field(bits, p)
+        self.field = Field(bits, p, strategy)  # "montgomery" for full-width primes
         K = self.field.limbs
         self.K = K
 
@@ -240,11 +241,13 @@ class DeviceBackend:
 class FourStepNtt:
     """One length-n NTT across the ranks of a communicator (see module doc)."""
 
-    def __init__(self, bits: int, params: NttParams, rank: int, world: int, backend=None, comm=None):
+    def __init__(self, bits: int, params: NttParams, rank: int, world: int, backend=None, comm=None,
+                 strategy: str = "schoolbook"):
         self.params = params
         self.layout = FourStepLayout(params.n, *split_lengths(params.n), world)
         self.rank, self.world = rank, world
-        self.backend = backend if backend is not None else DeviceBackend(bits, params, self.layout, rank)
+        self.backend = (backend if backend is not None
+                        else DeviceBackend(bits, params, self.layout, rank, strategy))
         self.comm = comm
 
     # phase 1: local row transforms + twiddle/transpose -> send buffer

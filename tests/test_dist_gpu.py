@@ -63,6 +63,34 @@ def test_loopback_fused_exchange_matches_nccl_form(cuda, logn, P):
         assert torch.equal(back[r], xs[r])
 
 
+def test_loopback_full_width_field(cuda):
+    """The distributed four-step over a full-width (Montgomery) field:
+    BLS12-381 r at 256 bits, both exchange forms, against the single-GPU plan."""
+    import torch
+    from paper_2501_07535_b200 import device as dev
+    from paper_2501_07535_b200 import dist as D
+    from paper_2501_07535_b200.params import NttParams
+    r = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+    n, P = 1 << 16, 4
+    w = pow(7, (r - 1) // n, r)
+    prm = NttParams(n=n, p=r, root=w, root_inv=pow(w, -1, r), n_inv=pow(n, -1, r))
+    engines = [D.FourStepNtt(256, prm, k, P, strategy="montgomery") for k in range(P)]
+    L = engines[0].layout
+    g = torch.Generator(device="cuda").manual_seed(381)
+    x = torch.randint(-(1 << 31), 1 << 31, (n, 8), dtype=torch.int32, device="cuda", generator=g)
+    x[:, 7] &= (1 << 28) - 1
+    xs = [L.scatter_input(x, k) for k in range(P)]
+    ys = D.loopback_transform(engines, xs)
+    yf = D.loopback_transform_fused(engines, xs)
+    want = dev.NttPlan(dev.Field(256, r, "montgomery"), prm).forward(x).cpu().numpy()
+    assert np.array_equal(L.gather_output([t.cpu().numpy() for t in ys]), want)
+    for a, b in zip(ys, yf):
+        assert torch.equal(a, b)
+    back = D.loopback_transform_fused(engines, yf, inverse=True)
+    for k in range(P):
+        assert torch.equal(back[k], xs[k])
+
+
 def test_scatter_argument_errors(cuda):
     import torch
     from paper_2501_07535_b200 import _lib
