@@ -36,14 +36,14 @@ int cuda_fail(cudaError_t e, const char *what);
 // ------------------------------------------------------------------ limb sets
 // Limb counts compiled into the library.  K = ceil(bits/32).
 #ifndef WM_BLAS_KS
-#define WM_BLAS_KS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(16) X(24) X(32)
+#define WM_BLAS_KS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(24) X(32)
 #endif
 // Full-width (Montgomery) fields: the common curve / FHE sizes.
 #ifndef WM_MONT_KS
 #define WM_MONT_KS(X) X(1) X(2) X(4) X(8) X(12) X(16) X(24) X(32)
 #endif
 #ifndef WM_NTT_KS
-#define WM_NTT_KS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(12) X(16) X(24) X(32)
+#define WM_NTT_KS(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16) X(24) X(32)
 #endif
 
 bool blas_supports(int K);

@@ -14,7 +14,7 @@ from oracle.cbind import OracleField
 
 pytestmark = pytest.mark.gpu
 
-WIDTHS = [16, 32, 64, 96, 128, 160, 192, 224, 256, 288, 320, 352, 384, 512, 768, 1024]
+WIDTHS = [16, 32, 64, 96, 128, 160, 192, 224, 256, 288, 320, 352, 384, 416, 448, 480, 512, 768, 1024]
 
 
 def _dev():

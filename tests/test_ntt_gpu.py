@@ -71,7 +71,7 @@ def test_reference_2p16_checksums(cuda, golden):
         assert hashlib.sha256(yi.tobytes()).hexdigest() == row["inv_sha256"]
 
 
-@pytest.mark.parametrize("bits", [16, 32, 64, 96, 128, 192, 256, 384, 512, 768, 1024])
+@pytest.mark.parametrize("bits", [16, 32, 64, 96, 128, 192, 256, 288, 320, 352, 384, 416, 448, 480, 512, 768, 1024])
 @pytest.mark.parametrize("logn", [1, 2, 3, 5, 8, 10, 11, 12, 14])
 def test_sizes_and_widths_vs_c_oracle(cuda, bits, logn):
     """Every pass structure (1-3 passes) at every built width, batch 3, against
