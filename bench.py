@@ -767,6 +767,24 @@ def run_cpu_reference(transforms: int):
             "sample": f"{half} forward + {half} inverse transforms, C oracle port (oracle/ntt_oracle.c)"}
 
 
+def cpu_baseline_subprocess(args):
+    """The CPU baseline timed in a fresh process (the --impl reference arm's
+    code path): inside this process torch's OpenMP pool, left spinning by the
+    earlier host-side tensor work, competes with the reference's OpenMP
+    threads for the host cores (1.7x slower measured in-process)."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--steps", "3", "--warmup", "1",
+           "--ref-transforms", str(2 * max(1, args.cpu_sample // 2))]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    try:
+        res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
+        line = json.loads(res.stdout.strip().splitlines()[-1])
+        cb = line["cpu_baseline"]
+        cb["process"] = "fresh subprocess (bench.py --impl reference --steps 3 --warmup 1)"
+        return cb
+    except Exception as exc:  # report, do not fail the bench
+        return {"value": None, "unit": UNIT, "cores": None, "kind": "unavailable", "sample": str(exc)[:200]}
+
+
 def reference_arm(args, rank, world, pg):
     """--impl reference: the reference's CPU implementation of the path."""
     if rank != 0:
@@ -786,7 +804,7 @@ def reference_arm(args, rank, world, pg):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": wall * 1e3 / args.steps, "higher_is_better": False, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": {"workload": "256-bit forward+inverse NTT n=2^16 (sample of the batch-64 step)",
+        "config": {"workload": "256-bit forward+inverse NTT n=2^16 batch 64 (BASELINE configs[1]); --ref-transforms per step, default the whole 64+64 step",
                    "bits": BITS, "n": N, "transforms_per_step": 2 * (per_step // 2)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
                          "sample": r["sample"]},
@@ -810,9 +828,10 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-transforms", type=int, default=32,
-                    help="transforms per reference-arm step (a bounded sample of the 128)")
-    ap.add_argument("--cpu-sample", type=int, default=16)
+    ap.add_argument("--ref-transforms", type=int, default=2 * BATCH,
+                    help="transforms per reference-arm step (default: the whole 64 fwd + 64 inv step)")
+    ap.add_argument("--cpu-sample", type=int, default=2 * BATCH,
+                    help="transforms per CPU-baseline step (default: the whole batch-64 fwd+inv step)")
     ap.add_argument("--skip-extras", action="store_true", help="only the headline workload")
     ap.add_argument("--blas-bits", type=int, nargs="*", default=[128, 256, 384, 768])
     ap.add_argument("--e2e-chunk", type=int, default=0, help="transforms per host-pipeline chunk (0 = auto)")
@@ -876,10 +895,7 @@ def main():
     }
     cpu = None
     if world == 1:
-        try:
-            cpu = run_cpu_reference(args.cpu_sample)
-        except Exception as exc:  # report, do not fail the bench
-            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "unavailable", "sample": str(exc)}
+        cpu = cpu_baseline_subprocess(args)
     out = {
         "metric": METRIC,
         "value": res["us_per_transform"],
