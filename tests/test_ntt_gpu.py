@@ -238,3 +238,21 @@ def test_host_pipeline_reference_layout(cuda, mode):
         else:  # forward_inverse round trip, or the copy-only pipeline
             want = xd
         assert got == dev.limbs_to_ints(dev.to_host(want)), chunk
+
+
+def test_host_pipeline_ramped_chunks(cuda):
+    """Auto chunking at n = 2^16 (8 MiB chunks of 4 transforms, halved to 2
+    and 1 at both ends): batch 13 -> chunks 1,2,4,3,2,1; in place."""
+    dev = _dev()
+    import torch
+    n, batch = 1 << 16, 13
+    plan = plan_for(256, n)
+    g = torch.Generator(device="cuda").manual_seed(13)
+    x = torch.randint(-(1 << 31), 1 << 31, (batch * n, 8), dtype=torch.int32, device="cuda", generator=g)
+    x[:, 7] &= (1 << 27) - 1
+    ref = plan.field.to_ref_layout(x, 64, 4).cpu().pin_memory()
+    buf = ref.clone().pin_memory()
+    plan.host_transform(buf, buf, mode="forward", word_bits=64, ref_words=4)
+    torch.cuda.synchronize()
+    want = plan.field.to_ref_layout(plan.forward(x), 64, 4).cpu()
+    assert torch.equal(buf, want)
