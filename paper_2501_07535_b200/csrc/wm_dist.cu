@@ -198,11 +198,10 @@ template <int K, bool MONT>
 static int launch_scale_transpose_t(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out,
                                     int64_t rows, int64_t cols, cudaStream_t st, const ScatterDst &D) {
   const size_t smem = (size_t)TT * (TT * K + 1) * 4;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
     WM_CUDA_TRY(cudaFuncSetAttribute(scale_transpose_kernel<K, MONT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)std::max<size_t>(smem, 48 * 1024)));
-    attr = true;
   }
   dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)((rows + TT - 1) / TT));
   scale_transpose_kernel<K, MONT><<<grid, 256, smem, st>>>(in, table, out, rows, cols, field_const<K>(f), D);
@@ -269,11 +268,9 @@ int wm_transpose(int words, const uint32_t *in, uint32_t *out, int64_t rows, int
     return WM_OK;
   }
   const size_t smem = (size_t)TT * (TT * words + 1) * 4;
-  static int attr_words = 0;
-  if (smem > 48 * 1024 && words > attr_words) {
+  if (smem > 48 * 1024) {  // (cheap; the attribute is per device and grows with `words`)
     WM_CUDA_TRY(cudaFuncSetAttribute(transpose_words_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
-    attr_words = words;
   }
   dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)((rows + TT - 1) / TT), (unsigned)batch);
   transpose_words_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(in, out, words, rows, cols);

@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstring>
 #include <mutex>
@@ -32,6 +33,15 @@ int cuda_fail(cudaError_t e, const char *what);
     cudaError_t _e = cudaGetLastError();                   \
     if (_e != cudaSuccess) return ::wm::cuda_fail(_e, what); \
   } while (0)
+
+// cudaFuncSetAttribute acts on the current device: attribute setup done once
+// per (call site, device).  Returns true the first time for the current device.
+inline bool first_on_device(std::atomic<uint64_t> &mask) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return true;
+  const uint64_t bit = 1ull << (dev & 63);
+  return (mask.fetch_or(bit) & bit) == 0;
+}
 
 // ------------------------------------------------------------------ limb sets
 // Limb counts compiled into the library.  K = ceil(bits/32).

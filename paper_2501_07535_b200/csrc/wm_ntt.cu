@@ -671,11 +671,10 @@ static size_t pass_smem(int K, const wm_pass_plan &ps) {
 template <int K, bool MONT>
 static int run_passes_t(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
                         uint32_t *ws, cudaStream_t st, int only_pass, const uint32_t *mul_by) {
-  static bool attr_done = false;
-  if (!attr_done) {
+  static std::atomic<uint64_t> attr_done{0};
+  if (first_on_device(attr_done)) {
     WM_CUDA_TRY(cudaFuncSetAttribute(ntt_col_pass<K, MONT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     WM_CUDA_TRY(cudaFuncSetAttribute(ntt_row_pass<K, MONT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_done = true;
   }
   const NttConst<K> c = ntt_const<K>(pl);
   for (int pi = 0; pi < (int)pl->passes.size(); ++pi) {
