@@ -18,12 +18,17 @@
 //     enough that a CTA holds G whole lines in shared memory.
 //   * A pass loads its G lines with coalesced vector loads (G consecutive
 //     columns of element-contiguous values), scatters them bit-reversed into
-//     shared memory, runs log2(L) radix-2 DIT stages there (Shoup multiply
-//     against a shared-memory twiddle table), applies the inter-pass twiddle
-//     root^(e) in the store epilogue, and writes with coalesced vector stores.
+//     an XOR-swizzled shared-memory tile, runs log2(L) radix-2 DIT stages
+//     there as radix-4 register groups (radix-2 at 24+ limbs; j-major group
+//     order so unit-twiddle warps skip their products), applies the
+//     inter-pass twiddle root^(e) in the store epilogue, and writes with
+//     coalesced vector stores.  The pass's twiddle sub-table arrives by one
+//     TMA bulk copy (cp.async.bulk + mbarrier) of a pre-swizzled image.
 //   * Twiddles are generated on the device once per plan as (w, w') pairs,
-//     w' = floor(w * 2^(32K) / p), so each butterfly multiply is a Shoup
-//     multiply (~K^2 + K^2/2 word products instead of the reference's 3K^2).
+//     w' = floor(w * 2^(32K) / p), so each butterfly multiply is a lazy Shoup
+//     multiply (~K^2 + K^2/2 word products instead of the reference's 3K^2),
+//     values in [0, 6p) until the last pass.  Full-width fields use
+//     Montgomery twiddles and canonical butterflies instead (Arith<K, true>).
 //   * For the inverse, n^-1 is folded into the last column pass's twiddle
 //     table (one-pass plans multiply by n^-1 in the epilogue instead).
 #include <algorithm>
