@@ -37,6 +37,16 @@ WM_DEV void ld8_stream(uint32_t *r, const uint32_t *p) {
                : "l"(p));
 }
 
+// Streaming (evict-first, no L1) loads when one access covers the element;
+// elements needing several accesses whose sectors are shared by neighbouring
+// lanes (e.g. 48-byte elements read as three 16-byte pieces) go through L1 so
+// the later pieces hit there.
+#ifndef WM_LD_L1_MULTI
+#define WM_LD_L1_MULTI 1  // A/B: 384-bit vadd 5.74 -> 6.40 TB/s (profiles/r01_ab_l1_multi_access.txt)
+#endif
+template <int K>
+constexpr bool kStreamLd = !(WM_LD_L1_MULTI && (K / VecWidth<K>::V) > 1);
+
 // Load element i (K limbs) from global memory.
 template <int K>
 WM_DEV void load_elem(uint32_t (&r)[K], const uint32_t *base, int64_t i) {
@@ -48,18 +58,20 @@ WM_DEV void load_elem(uint32_t (&r)[K], const uint32_t *base, int64_t i) {
   } else if constexpr (V == 4) {
 #pragma unroll
     for (int c = 0; c < K; c += 4) {
-      uint4 v = __ldcs(reinterpret_cast<const uint4 *>(p + c));
+      uint4 v = kStreamLd<K> ? __ldcs(reinterpret_cast<const uint4 *>(p + c))
+                              : __ldg(reinterpret_cast<const uint4 *>(p + c));
       r[c] = v.x; r[c + 1] = v.y; r[c + 2] = v.z; r[c + 3] = v.w;
     }
   } else if constexpr (V == 2) {
 #pragma unroll
     for (int c = 0; c < K; c += 2) {
-      uint2 v = __ldcs(reinterpret_cast<const uint2 *>(p + c));
+      uint2 v = kStreamLd<K> ? __ldcs(reinterpret_cast<const uint2 *>(p + c))
+                              : __ldg(reinterpret_cast<const uint2 *>(p + c));
       r[c] = v.x; r[c + 1] = v.y;
     }
   } else {
 #pragma unroll
-    for (int c = 0; c < K; ++c) r[c] = __ldcs(p + c);
+    for (int c = 0; c < K; ++c) r[c] = kStreamLd<K> ? __ldcs(p + c) : __ldg(p + c);
   }
 }
 
