@@ -320,10 +320,21 @@ int wm_abi_version(void) { return WM_ABI_VERSION; }
 
 const char *wm_last_error(void) { return g_last_error.c_str(); }
 
+// Storage limb count for K = ceil(bits/32): K itself when its kernels are
+// built, else the next limb count with full-width (Montgomery) kernels — such
+// widths run as zero-padded Montgomery fields (odd moduli).
+static int storage_limbs(int K) {
+  if (blas_supports(K)) return K;
+  int best = -1;
+#define WM_CASE(k) if (k >= K && (best < 0 || k < best)) best = k;
+  WM_MONT_KS(WM_CASE)
+#undef WM_CASE
+  return best;
+}
+
 int wm_limbs_for_bits(int bits) {
   if (bits < 1) return -1;
-  int K = (bits + 31) / 32;
-  return blas_supports(K) ? K : -1;
+  return storage_limbs((bits + 31) / 32);
 }
 
 int wm_supported_limbs(int ntt, int *out, int cap) {
@@ -352,8 +363,16 @@ int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags,
   if (bits < 8) return fail(WM_EINVAL, "width must be at least 8 bits");
   if (!q_host || q_limbs < 1) return fail(WM_EINVAL, "null modulus");
   int K = (bits + 31) / 32;
-  if (!blas_supports(K)) return fail(WM_EUNSUPPORTED, "width " + std::to_string(bits) + " (" +
-                                                          std::to_string(K) + " limbs) not built in");
+  if (!blas_supports(K)) {
+    // no kernels for this limb count: zero-pad to the next full-width
+    // (Montgomery) limb count; Montgomery needs an odd modulus
+    const int Kp = storage_limbs(K);
+    if (Kp < 0 || !(q_host[0] & 1u))
+      return fail(WM_EUNSUPPORTED, "width " + std::to_string(bits) + " (" + std::to_string(K) +
+                                       " limbs) not built in" + (Kp < 0 ? "" : " (padding needs an odd modulus)"));
+    K = Kp;
+    flags = (flags & ~WM_FIELD_KARATSUBA) | WM_FIELD_MONTGOMERY;
+  }
   Big q(q_host, q_host + q_limbs);
   for (int j = K; j < q_limbs; ++j)
     if (q[j]) return fail(WM_EINVAL, "modulus wider than the field width");

@@ -108,6 +108,9 @@ class Field:
         b, k, s = _i(), _i(), _i()
         _lib.check(self.lib.wm_field_info(self._h, ctypes.byref(b), ctypes.byref(k), ctypes.byref(s)))
         self.norm_shift = s.value
+        # storage limbs: ceil(bits/32), or the zero-padded limb count of a
+        # width without kernels of its own (run as a Montgomery field)
+        self.limbs = k.value
 
     @property
     def handle(self):

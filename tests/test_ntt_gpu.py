@@ -71,7 +71,7 @@ def test_reference_2p16_checksums(cuda, golden):
         assert hashlib.sha256(yi.tobytes()).hexdigest() == row["inv_sha256"]
 
 
-@pytest.mark.parametrize("bits", [16, 32, 64, 96, 128, 192, 256, 288, 320, 352, 384, 416, 448, 480, 512, 768, 1024])
+@pytest.mark.parametrize("bits", [16, 32, 64, 96, 128, 192, 256, 288, 320, 352, 384, 416, 448, 480, 512, 640, 768, 992, 1024])
 @pytest.mark.parametrize("logn", [1, 2, 3, 5, 8, 10, 11, 12, 14])
 def test_sizes_and_widths_vs_c_oracle(cuda, bits, logn):
     """Every pass structure (1-3 passes) at every built width, batch 3, against
@@ -87,14 +87,15 @@ def test_sizes_and_widths_vs_c_oracle(cuda, bits, logn):
     of = OracleField(prm.p, bits)
     batch = 3
     rng = np.random.Generator(np.random.PCG64(bits + logn))
-    xl = dev.ints_to_limbs(bigint.uniform_residues(rng, batch * n, prm.p), plan.limbs)
-    xd = dev.to_device(xl)
-    got = dev.to_host(plan.forward(xd))
-    want = of.ntt(xl, n, prm.root)
-    assert np.array_equal(got, want), (bits, n, "fwd")
-    got = dev.to_host(plan.inverse(xd))
-    want = of.ntt(xl, n, prm.root_inv, prm.n_inv)
-    assert np.array_equal(got, want), (bits, n, "inv")
+    vals = bigint.uniform_residues(rng, batch * n, prm.p)
+    kn = (bits + 31) // 32  # oracle limbs; the device may store zero-padded limbs
+    xl = dev.ints_to_limbs(vals, kn)
+    xd = dev.to_device(dev.ints_to_limbs(vals, plan.limbs))
+    for inverse in (False, True):
+        got = dev.to_host(plan.inverse(xd) if inverse else plan.forward(xd))
+        want = of.ntt(xl, n, prm.root_inv, prm.n_inv) if inverse else of.ntt(xl, n, prm.root)
+        assert np.array_equal(got[:, :kn], want), (bits, n, inverse)
+        assert not got[:, kn:].any(), (bits, n, "padding limbs")
 
 
 def test_2p20_vs_c_oracle(cuda):
