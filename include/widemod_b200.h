@@ -95,6 +95,13 @@ int wm_field_info(const wm_field *f, int *bits, int *limbs, int *norm_shift);
  * int n_elems)` (emit.py:456-484) for kind in vadd/vsub/vmul: out[i] =
  * a[i] (+,-,*) b[i] mod q for i < n.  out may alias a or b.
  * Semantics: reference build_vector kernels.py:215-256. */
+/* Replaces the reference's bare widening multiply `widemul_{bits}w{word}`
+ * (build_wide_mul kernels.py:314-329): out[i] = a[i] * b[i] as the full
+ * product, 2L limbs per element, where L = wm_limbs_for_bits(bits) is the
+ * storage limb count of a and b.  No modulus; karatsuba != 0 selects the
+ * Karatsuba full product (make_spec(..., strategy="karatsuba")). */
+int wm_widemul(int bits, int karatsuba, const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n,
+               void *stream);
 int wm_vadd(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out,
             int64_t n, void *stream);
 int wm_vsub(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out,

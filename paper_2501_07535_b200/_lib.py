@@ -68,6 +68,7 @@ SIGNATURES = [
     ("wm_ntt_host", _int, [_vp, _int, _int, _int, _vp, _vp, _i64, _i64, _vp]),
     ("wm_transpose", _int, [_int, _vp, _vp, _i64, _i64, _i64, _vp]),
     ("wm_scale_transpose", _int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp]),
+    ("wm_widemul", _int, [_int, _int, _vp, _vp, _vp, _i64, _vp]),
     ("wm_scale_transpose_scatter", _int, [_vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _i64, _i64, _vp]),
     ("wm_twiddle_table_2d", _int, [_vp, _i64, _u32p, _i64, _i64, _i64, _vp, _vp]),
     ("wm_ref_to_limbs", _int, [_int, _int, _int, _vp, _vp, _i64, _vp]),

@@ -276,6 +276,31 @@ static int blas_dispatch(int op, const wm_field *f, const uint32_t *a, const uin
   }
 }
 
+// ------------------------------------------------------------------ widemul
+// out[i] = a[i] * b[i], the full 2K-limb product (reference build_wide_mul,
+// kernels.py:314-329: the bare widening multiply, no modulus).
+template <int K, int STRAT>
+__global__ void __launch_bounds__(256) widemul_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
+                                                      int64_t n) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    uint32_t x[K], y[K], t[2 * K];
+    load_elem<K>(x, a, i);
+    load_elem<K>(y, b, i);
+    mul_full_s<K, barrett_style<K>(), STRAT>(t, x, y);
+    store_elem<2 * K>(out, i, t);
+  }
+}
+
+template <int K, int STRAT>
+static int launch_widemul(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, cudaStream_t st) {
+  int64_t want = (n + 255) / 256;
+  int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, 148 * 8));
+  widemul_kernel<K, STRAT><<<grid, 256, 0, st>>>(a, b, out, n);
+  WM_LAUNCH_CHECK("widemul_kernel launch");
+  return WM_OK;
+}
+
 // ------------------------------------------------------------------ layout
 __global__ void ref_to_limbs_kernel(int word_bits, int R, int K, const void *ref, uint32_t *out, int64_t total) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -452,6 +477,26 @@ int wm_field_info(const wm_field *f, int *bits, int *limbs, int *norm_shift) {
   if (limbs) *limbs = f->K;
   if (norm_shift) *norm_shift = f->s;
   return WM_OK;
+}
+
+int wm_widemul(int bits, int karatsuba, const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n,
+               void *stream) {
+  if (bits < 1) return fail(WM_EINVAL, "bad width");
+  if (n < 0) return fail(WM_EINVAL, "negative length");
+  if (n == 0) return WM_OK;
+  if (!a || !b || !out) return fail(WM_EINVAL, "null data pointer");
+  const int K = storage_limbs((bits + 31) / 32);
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (K) {
+#define WM_CASE(k)                                                                          \
+  case k:                                                                                   \
+    return karatsuba ? launch_widemul<k, kKaratsuba>(a, b, out, n, st)                      \
+                     : launch_widemul<k, kSchoolbook>(a, b, out, n, st);
+    WM_BLAS_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      return fail(WM_EUNSUPPORTED, "width not built into the widemul kernel");
+  }
 }
 
 int wm_vadd(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, void *stream) {

@@ -173,12 +173,18 @@ class DeviceKernel:
     def __init__(self, spec: KernelSpec, params_mode: str = "baked"):
         if params_mode not in PARAMS_MODES:
             raise InvalidKernel(f"unknown params mode {params_mode!r}")
-        if spec.kind == "widemul":
-            raise InvalidKernel("widemul is not a device kernel (only modular ops are on the hot path)")
         self.spec = spec
         self.kind = spec.kind
         lay = spec.layout
         bp = spec.barrett
+        if spec.kind == "widemul":  # bare widening multiply (kernels.py:314-329), no modulus
+            self.name = f"widemul_{lay.bits}w{lay.word_bits}"
+            self.attributes = _Attrs({
+                "kernel": "widemul", "lambda": lay.bits, "omega0": lay.word_bits,
+                "level_bits": lay.word_bits, "padded_bits": lay.padded_bits, "n": 1,
+                "params_mode": params_mode, "limbs": lay.limbs, "arg_names": ["a", "b"],
+                "ret_names": ["c"], "vector_args": [True, True]}, twiddle_source=None)
+            return
         attrs = {
             "kernel": spec.kind,
             "lambda": lay.bits,
@@ -220,6 +226,8 @@ class DeviceKernel:
 
     @property
     def modulus(self) -> int:
+        if self.spec.barrett is None:
+            raise InvalidKernel(f"{self.kind} has no modulus")
         return self.spec.ntt.p if self.spec.ntt is not None else self.spec.barrett.q
 
     def field(self) -> Field:
@@ -334,11 +342,37 @@ def _vector_launch(kern: DeviceKernel, op: str, arrays) -> list[int]:
     return limbs_to_ints(to_host(out))
 
 
+def _widemul_launch(kern: DeviceKernel, xs, ys) -> list[int]:
+    """Full products a*b on the device (C ABI wm_widemul); operands are
+    unsigned values below 2^(32 * storage limbs)."""
+    from . import _lib
+    from .device import _stream_ptr, _torch
+    torch = _torch()
+    bits = kern.spec.layout.bits
+    lib = _lib.load()
+    K = lib.wm_limbs_for_bits(bits)
+    if K < 1:
+        raise _lib.Unsupported(f"width {bits} not built")
+    for v in list(xs) + list(ys):
+        if not 0 <= v < (1 << (32 * K)):
+            raise ValueError(f"widemul operand {v} does not fit {bits} bits")
+    x = to_device(ints_to_limbs(xs, K))
+    y = to_device(ints_to_limbs(ys, K))
+    out = torch.empty((len(xs), 2 * K), dtype=torch.int32, device="cuda")
+    _lib.check(lib.wm_widemul(bits, 1 if kern.spec.mul_strategy == "karatsuba" else 0, x.data_ptr(),
+                              y.data_ptr(), out.data_ptr(), len(xs), _stream_ptr(None)), "wm_widemul")
+    return limbs_to_ints(to_host(out))
+
+
 def run_program(program: DeviceKernel, *args, fn=None):
     """Run a kernel on single operands (reference kernels.py:442-464).
     Scalar kinds take (a, b); vector kinds take one element per argument;
     transforms take (u, v, w) and return the butterfly (u + v*w, u - v*w)."""
     kind = program.kind
+    if kind == "widemul":
+        if len(args) != 2:
+            raise TypeError(f"{len(args)} operands for 2 parameters")
+        return _widemul_launch(program, [args[0]], [args[1]])[0]
     if kind in SCALAR_KINDS or kind in ("vadd", "vsub", "vmul"):
         if len(args) != 2:
             raise TypeError(f"{len(args)} operands for 2 parameters")
@@ -367,6 +401,12 @@ def run_vector(program: DeviceKernel, *arrays, fn=None) -> list[int]:
     arrays are (a, b) for vadd/vsub/vmul and (a_scalar, x, y) for axpy;
     ValueError on a length mismatch."""
     attrs = program.attributes
+    if program.kind == "widemul":  # the reference maps run_program over the elements
+        if len(arrays) != 2:
+            raise TypeError(f"{len(arrays)} operands for 2 parameters")
+        if len(arrays[0]) != len(arrays[1]):
+            raise ValueError(f"expected {len(arrays[0])} elements, got {len(arrays[1])}")
+        return _widemul_launch(program, arrays[0], arrays[1])
     if program.kind not in VECTOR_KINDS:
         raise InvalidKernel(f"{program.kind} is not a vector kernel")
     n = attrs["n"]

@@ -69,8 +69,10 @@ def test_generate_kernel_attributes():
     assert [int(x) for x in nt.attributes["twiddles"]] == K.twiddle_table(find_ntt_params(16, 8), inverse=True)
     with pytest.raises(K.InvalidKernel):
         K.generate_kernel(K.make_spec("vadd", 16, 8, size=4), params_mode="wat")
+    wm = K.generate_kernel(K.make_spec("widemul", 64, 8))  # reference build_wide_mul kernels.py:314-329
+    assert wm.name == "widemul_64w8" and wm.attributes["ret_names"] == ["c"]
     with pytest.raises(K.InvalidKernel):
-        K.generate_kernel(K.make_spec("widemul", 64, 8))
+        wm.modulus
 
 
 def test_run_vector_validation_before_launch():  # reference test_kernels.py:137-144

@@ -205,3 +205,20 @@ def test_ref_layout_roundtrip(cuda):
 def find_prime_below(bits):
     from paper_2501_07535_b200.params import find_ntt_params
     return find_ntt_params(bits, 1).p
+
+
+def test_widemul_full_products(cuda):
+    """Bare widening multiply (reference build_wide_mul, kernels.py:314-329):
+    test_kernels.py:266-269 pins plus random operands at several widths and
+    both strategies."""
+    from paper_2501_07535_b200 import kernels as K
+    prog = K.generate_kernel(K.make_spec("widemul", 16, 8))
+    assert K.run_program(prog, 0xFFFF, 0xFFFF) == 0xFFFF * 0xFFFF
+    assert K.run_program(prog, 1234, 4321) == 1234 * 4321
+    rnd = random.Random(5)
+    for bits in (64, 256, 384, 640, 1024):
+        for strat in ("schoolbook", "karatsuba"):
+            wm = K.generate_kernel(K.make_spec("widemul", bits, 32, strategy=strat))
+            xs = [rnd.getrandbits(bits) for _ in range(500)] + [(1 << bits) - 1, 0, 1]
+            ys = [rnd.getrandbits(bits) for _ in range(500)] + [(1 << bits) - 1, (1 << bits) - 1, 1]
+            assert K.run_vector(wm, xs, ys) == [a * b for a, b in zip(xs, ys)], (bits, strat)
