@@ -365,8 +365,8 @@ def run_blas(args, torch, _field, pg):
         a[:, K - 1] &= top
         b[:, K - 1] &= top
         out = torch.empty_like(a)
-        # multiplier strategy per width: Karatsuba wins from 12 limbs up (tools/ab_timing.py)
-        fk = dev.Field(bits, q, "karatsuba") if K >= 12 else f
+        # multiplier strategy per width: Karatsuba wins from 8 limbs up (profiles/r01_ab_blas_mid_occupancy.txt)
+        fk = dev.Field(bits, q, "karatsuba") if K >= 8 else f
         for op in ("vadd", "vmul", "axpy"):
             fm = fk if op in ("vmul", "axpy") else f
             fn = (lambda: fm.axpy(123456789, a, b, out=out)) if op == "axpy" else \

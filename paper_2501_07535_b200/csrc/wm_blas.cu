@@ -164,9 +164,12 @@ constexpr int kMontField = 2;
 #ifndef WM_BLAS_MINB_WIDE  // resident CTAs requested for K >= 16 (register cap)
 #define WM_BLAS_MINB_WIDE 1
 #endif
+#ifndef WM_BLAS_MINB_MID  // 9 <= K <= 15: 3 CTAs/SM (<= 85 registers)
+#define WM_BLAS_MINB_MID 3
+#endif
 
 template <int K, int OP, int STRAT>
-__global__ void __launch_bounds__(256, (K >= 16 ? WM_BLAS_MINB_WIDE : 1)) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
+__global__ void __launch_bounds__(256, (K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? WM_BLAS_MINB_MID : 1)) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
                                                    int64_t n, const __grid_constant__ BlasArgs<K> args) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
