@@ -48,8 +48,14 @@
 #ifndef WM_NTT_MINB_WIDE  // K > 12: 2 CTAs/SM with a few spilled registers beat
 #define WM_NTT_MINB_WIDE 2   // 1 CTA/SM (profiles/r01_ab_wide_occupancy.txt: 768-bit 102 -> 91 us)
 #endif
-#define WM_NTT_BOUNDS(K) \
-  __launch_bounds__(256, ((K) <= 4 ? WM_NTT_MINB_SMALL : (K) <= 12 ? WM_NTT_MINB : WM_NTT_MINB_WIDE))
+#ifndef WM_NTT_MINB_MONT  // full-width (Montgomery) kernels, K <= 8
+#define WM_NTT_MINB_MONT 2
+#endif
+#define WM_NTT_BOUNDS(K, MONT)                                                                      \
+  __launch_bounds__(256, ((MONT) && (K) <= 8 ? WM_NTT_MINB_MONT                                   \
+                          : (K) <= 4         ? WM_NTT_MINB_SMALL                                  \
+                          : (K) <= 12        ? WM_NTT_MINB                                        \
+                                             : WM_NTT_MINB_WIDE))
 // Target tile size (32-bit words of data per CTA; 16384 = 64 KB).
 #ifndef WM_NTT_TILE_WORDS
 #define WM_NTT_TILE_WORDS 16384
@@ -407,7 +413,7 @@ __global__ void twiddle_image_kernel(const uint32_t *table, int64_t stride, int 
 // ------------------------------------------------------------------ column pass
 // Line (o, i), i in [0, lines_inner) consecutive per CTA (G of them).
 template <int K, bool MONT>
-__global__ void WM_NTT_BOUNDS(K) ntt_col_pass(const uint32_t *in, uint32_t *out,
+__global__ void WM_NTT_BOUNDS(K, MONT) ntt_col_pass(const uint32_t *in, uint32_t *out,
                                                     const uint32_t *tw_out, const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -495,7 +501,7 @@ __global__ void WM_NTT_BOUNDS(K) ntt_col_pass(const uint32_t *in, uint32_t *out,
 // ------------------------------------------------------------------ row pass
 // Line lambda in [0, batch * lines_inner): b = lambda / R, r = lambda % R.
 template <int K, bool MONT>
-__global__ void WM_NTT_BOUNDS(K) ntt_row_pass(const uint32_t *in, uint32_t *out,
+__global__ void WM_NTT_BOUNDS(K, MONT) ntt_row_pass(const uint32_t *in, uint32_t *out,
                                                     const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
