@@ -660,7 +660,10 @@ WM_DEV void mul_barrett_full(uint32_t (&r)[K], const uint32_t (&a)[K], const uin
   uint32_t as[K];
   shl_small<K>(as, a, F.s);
   uint32_t t[2 * K];
-  mul_full<K, kU64>(t, as, b);
+#ifndef WM_FULLBAR_KARA_FROM
+#define WM_FULLBAR_KARA_FROM 12  // profiles/r01_ab_fullwidth_karatsuba.txt (768-bit +10 %, 256-bit -1 %)
+#endif
+  mul_full_s<K, kU64, (K >= WM_FULLBAR_KARA_FROM ? kKaratsuba : kSchoolbook)>(t, as, b);
   // q1 = t >> (32K - 1)
   uint32_t q1[K];
 #pragma unroll
