@@ -223,8 +223,8 @@ def run_gpu(args, rank, world, local, pg):
             step()
             ev[s][1].record(stream)
         torch.cuda.synchronize()
-        # the dominant kernel alone (pass 0 = ntt_col_pass, 45% of the step in the
-        # ncu launch list profiles/r01_launches_bench.csv), for the roofline
+        # the dominant kernel alone (pass 0 = ntt_col_pass: its forward and inverse
+        # launches are ~55% of the step, profiles/r01_launch_share.json), for the roofline
         for s in range(args.steps):
             flush_l2(torch, flush)
             fwd_ev[s][0].record(stream)
