@@ -119,6 +119,7 @@ struct wm_ntt_plan {
   uint32_t *tw_img = nullptr;
   std::vector<size_t> tw_img_off;
   size_t tw_img_words_dir = 0;
+  int mode = 0;        // Arith mode: 0 lazy Shoup [0,6p), 1 Montgomery, 2 Shoup [0,4p) (full-width p < 2^(32K-2))
   wm::Big ninv_mont;  // full-width fields: n^-1 R mod p (one-pass inverse scale)
   wm::Big ninv, ninv_sh, np, p2, p3, p4;  // n^-1, floor(n^-1 * 2^32K / p), 2^32K - p, 2p, 3p, 4p
   // internal workspace (used when the caller passes none)

@@ -51,8 +51,8 @@
 #ifndef WM_NTT_MINB_MONT  // full-width (Montgomery) kernels, K <= 8
 #define WM_NTT_MINB_MONT 2
 #endif
-#define WM_NTT_BOUNDS(K, MONT)                                                                      \
-  __launch_bounds__(256, ((MONT) && (K) <= 8 ? WM_NTT_MINB_MONT                                   \
+#define WM_NTT_BOUNDS(K, MODE)                                                                      \
+  __launch_bounds__(256, ((MODE) == 1 && (K) <= 8 ? WM_NTT_MINB_MONT                              \
                           : (K) <= 4         ? WM_NTT_MINB_SMALL                                  \
                           : (K) <= 12        ? WM_NTT_MINB                                        \
                                              : WM_NTT_MINB_WIDE))
@@ -94,16 +94,19 @@ struct PassDesc {
 };
 
 // ------------------------------------------------------------------ arithmetic policy
-// MONT = false: reference-range fields (p < 2^(32K-4)): Shoup twiddle
-// products (tables hold (w, w')), lazy values in [0, 6p), canonical at the end.
-// MONT = true: full-width fields (WM_FIELD_MONTGOMERY, any odd p < 2^(32K)):
+// MODE 0: reference-range fields (p < 2^(32K-4)): Shoup twiddle products
+// (tables hold (w, w')), lazy values in [0, 6p), canonical at the end.
+// MODE 1: full-width fields (WM_FIELD_MONTGOMERY, any odd p < 2^(32K)):
 // tables hold w R mod p, each product is a Montgomery product, values stay
 // canonical (no headroom above p for a lazy window).
-template <int K, bool MONT>
+// MODE 2: full-width fields with p < 2^(32K-2) (BN254 r, BLS12-377 r, ...):
+// Shoup products and Harvey's [0, 4p) window (two conditional subtractions
+// per butterfly instead of a Montgomery product's extra K^2/2 products).
+template <int K, int MODE>
 struct Arith;
 
 template <int K>
-struct Arith<K, false> {
+struct Arith<K, 0> {
   static constexpr bool kWp = true;
   WM_DEV static void bf(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&wp)[K],
                         const NttConst<K> &c) {
@@ -121,7 +124,7 @@ struct Arith<K, false> {
 };
 
 template <int K>
-struct Arith<K, true> {
+struct Arith<K, 1> {
   static constexpr bool kWp = false;
   WM_DEV static void finish(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&t)[K], const NttConst<K> &c) {
     uint32_t a[K], b[K];
@@ -146,6 +149,44 @@ struct Arith<K, true> {
     mont_mul<K>(r, v, w, c.p, c.F.qinv);
   }
   WM_DEV static void canon(uint32_t (&)[K], const NttConst<K> &) {}
+  WM_DEV static void mulby(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&m)[K], const NttConst<K> &c) {
+    mul_mont_plain<K>(r, v, m, c.F);
+  }
+};
+
+template <int K>
+struct Arith<K, 2> {
+  static constexpr bool kWp = true;
+  // u in [0, 4p) -> [0, 2p); t in [0, 2p); x0 = u + t, x1 = u + 2p - t, both in [0, 4p)
+  WM_DEV static void finish(uint32_t (&x0)[K], uint32_t (&x1)[K], uint32_t (&t)[K], const NttConst<K> &c) {
+    uint32_t u[K], a[K];
+    copy_n<K>(u, x0);
+    cond_sub<K>(u, c.p2);
+    add_n<K>(x0, u, t);
+    add_n<K>(a, u, c.p2);
+    sub_n<K>(x1, a, t);
+  }
+  WM_DEV static void bf(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&wp)[K],
+                        const NttConst<K> &c) {
+    uint32_t t[K];
+    mul_shoup_lazy<K>(t, x1, w, wp, c.np);  // [0, 3p)
+    cond_sub<K>(t, c.p2);                   // [0, 2p)
+    finish(x0, x1, t, c);
+  }
+  WM_DEV static void bf1(uint32_t (&x0)[K], uint32_t (&x1)[K], const NttConst<K> &c) {
+    uint32_t t[K];
+    copy_n<K>(t, x1);
+    cond_sub<K>(t, c.p2);
+    finish(x0, x1, t, c);
+  }
+  WM_DEV static void twmul(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
+                           const uint32_t (&wp)[K], const NttConst<K> &c) {
+    mul_shoup_lazy<K>(r, v, w, wp, c.np);  // [0, 3p) within the window
+  }
+  WM_DEV static void canon(uint32_t (&v)[K], const NttConst<K> &c) {
+    cond_sub<K>(v, c.p2);
+    cond_sub<K>(v, c.p);
+  }
   WM_DEV static void mulby(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&m)[K], const NttConst<K> &c) {
     mul_mont_plain<K>(r, v, m, c.F);
   }
@@ -209,13 +250,13 @@ struct Smem {
 // ------------------------------------------------------------------ in-smem DFT
 // One radix-4 group (stages s, s+1) with one product at a time (wide K,
 // where two interleaved products would spill registers).
-template <int K, bool MONT>
+template <int K, int MODE>
 __device__ __forceinline__ void radix4_single(uint32_t (&x0)[K], uint32_t (&x1)[K], uint32_t (&x2)[K],
                                               uint32_t (&x3)[K], const uint32_t *tww, const uint32_t *twp, int s,
                                               int j, int h, int logL, int lq, bool trivial,
                                               const NttConst<K> &c) {
   using S = Smem<K>;
-  using A = Arith<K, MONT>;
+  using A = Arith<K, MODE>;
   uint32_t w[K], wp[K];
   if (trivial) {  // j == 0: the stage-s twiddle and the first stage-(s+1) twiddle are 1
     A::bf1(x0, x1, c);
@@ -255,11 +296,11 @@ __host__ __device__ constexpr bool ntt_radix2() {
   return K >= WM_NTT_RADIX2_FROM;
 }
 
-template <int K, bool MONT>
+template <int K, int MODE>
 __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, const uint32_t *twp, int logL,
                                          int G, const NttConst<K> &c) {
   using S = Smem<K>;
-  using A = Arith<K, MONT>;
+  using A = Arith<K, MODE>;
   const int L = 1 << logL;
   if constexpr (ntt_radix2<K>()) {
   for (int s = 0; s < logL; ++s) {
@@ -332,7 +373,7 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
       S::load(x1, data, e0 + h);
       S::load(x2, data, e0 + 2 * h);
       S::load(x3, data, e0 + 3 * h);
-      radix4_single<K, MONT>(x0, x1, x2, x3, tww, twp, s, j, h, logL, lq, s == 0 || (jmajor && j == 0), c);
+      radix4_single<K, MODE>(x0, x1, x2, x3, tww, twp, s, j, h, logL, lq, s == 0 || (jmajor && j == 0), c);
 
       S::store(data, e0, x0);
       S::store(data, e0 + h, x1);
@@ -412,8 +453,8 @@ __global__ void twiddle_image_kernel(const uint32_t *table, int64_t stride, int 
 
 // ------------------------------------------------------------------ column pass
 // Line (o, i), i in [0, lines_inner) consecutive per CTA (G of them).
-template <int K, bool MONT>
-__global__ void WM_NTT_BOUNDS(K, MONT) ntt_col_pass(const uint32_t *in, uint32_t *out,
+template <int K, int MODE>
+__global__ void WM_NTT_BOUNDS(K, MODE) ntt_col_pass(const uint32_t *in, uint32_t *out,
                                                     const uint32_t *tw_out, const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -455,7 +496,7 @@ __global__ void WM_NTT_BOUNDS(K, MONT) ntt_col_pass(const uint32_t *in, uint32_t
   }
   __syncthreads();
   twimg_wait(mbar);
-  dft_smem<K, MONT>(data, tww, twp, logL, G, c);
+  dft_smem<K, MODE>(data, tww, twp, logL, G, c);
   // inter-pass twiddle exponent, reduced mod n (n | 2^32, so 32-bit wraparound is exact)
   const uint32_t nmask = (uint32_t)(d.n - 1);
   const uint32_t oc1 = (uint32_t)(o * d.C1);
@@ -470,7 +511,7 @@ __global__ void WM_NTT_BOUNDS(K, MONT) ntt_col_pass(const uint32_t *in, uint32_t
         const uint32_t e = ((uint32_t)((i0 + g) >> d.SH) * (oc1 + (uint32_t)k * (uint32_t)d.C2) *
                             (uint32_t)d.C3) & nmask;
         ldg_elem<K>(w[u], tw_out + (size_t)e * (2 * K));
-        if constexpr (Arith<K, MONT>::kWp) ldg_elem<K>(wp[u], tw_out + (size_t)e * (2 * K) + K);
+        if constexpr (Arith<K, MODE>::kWp) ldg_elem<K>(wp[u], tw_out + (size_t)e * (2 * K) + K);
       }
     }
 #pragma unroll
@@ -482,15 +523,15 @@ __global__ void WM_NTT_BOUNDS(K, MONT) ntt_col_pass(const uint32_t *in, uint32_t
       S::load(v, data, g * L + k);
       if (d.C3) {
         uint32_t r[K];
-        Arith<K, MONT>::twmul(r, v, w[u], wp[u], c);
+        Arith<K, MODE>::twmul(r, v, w[u], wp[u], c);
         copy_n<K>(v, r);
       }
-      if (d.canonical_out) Arith<K, MONT>::canon(v, c);
+      if (d.canonical_out) Arith<K, MODE>::canon(v, c);
       const int64_t off = (((int64_t)k << d.logWK) + g) * K;
       if (d.mul_by) {
         uint32_t m[K], rr[K];
         ldg_elem<K>(m, d.mul_by + (dst - out) + off);
-        Arith<K, MONT>::mulby(rr, v, m, c);
+        Arith<K, MODE>::mulby(rr, v, m, c);
         copy_n<K>(v, rr);
       }
       stg_elem<K>(dst + off, v);
@@ -500,8 +541,8 @@ __global__ void WM_NTT_BOUNDS(K, MONT) ntt_col_pass(const uint32_t *in, uint32_t
 
 // ------------------------------------------------------------------ row pass
 // Line lambda in [0, batch * lines_inner): b = lambda / R, r = lambda % R.
-template <int K, bool MONT>
-__global__ void WM_NTT_BOUNDS(K, MONT) ntt_row_pass(const uint32_t *in, uint32_t *out,
+template <int K, int MODE>
+__global__ void WM_NTT_BOUNDS(K, MODE) ntt_row_pass(const uint32_t *in, uint32_t *out,
                                                     const __grid_constant__ PassDesc d,
                                                     const __grid_constant__ NttConst<K> c) {
   extern __shared__ __align__(16) uint32_t smem[];
@@ -537,7 +578,7 @@ __global__ void WM_NTT_BOUNDS(K, MONT) ntt_row_pass(const uint32_t *in, uint32_t
   }
   __syncthreads();
   twimg_wait(mbar);
-  dft_smem<K, MONT>(data, tww, twp, logL, G, c);
+  dft_smem<K, MODE>(data, tww, twp, logL, G, c);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
     const int g = idx >> logL, k = idx & (L - 1);
     const int64_t lam = lam0 + g;
@@ -547,15 +588,15 @@ __global__ void WM_NTT_BOUNDS(K, MONT) ntt_row_pass(const uint32_t *in, uint32_t
       S::load(v, data, g * L + k);
       if (d.scale_out) {
         uint32_t rr[K];
-        Arith<K, MONT>::twmul(rr, v, c.sc, c.scp, c);
+        Arith<K, MODE>::twmul(rr, v, c.sc, c.scp, c);
         copy_n<K>(v, rr);
       }
-      if (d.canonical_out) Arith<K, MONT>::canon(v, c);
+      if (d.canonical_out) Arith<K, MODE>::canon(v, c);
       const int64_t pos = (b << d.logn) + (r << d.logWO) + ((int64_t)k << d.logWK);
       if (d.mul_by) {  // fused pointwise product (NTT-domain convolution)
         uint32_t m[K], rr[K];
         ldg_elem<K>(m, d.mul_by + pos * K);
-        Arith<K, MONT>::mulby(rr, v, m, c);
+        Arith<K, MODE>::mulby(rr, v, m, c);
         copy_n<K>(v, rr);
       }
       stg_elem<K>(out + pos * K, v);
@@ -579,7 +620,7 @@ WM_DEV void tw_mul(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)
   if constexpr (MONT) mont_mul<K>(r, a, b, F.q, F.qinv); else mul_barrett<K>(r, a, b, F);
 }
 
-template <int K, bool MONT>
+template <int K, bool MONT, bool PLAIN = false>
 __global__ void twiddle_gen_kernel(uint32_t *table, int64_t count, const __grid_constant__ TwGenArgs<K> a) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t e0 = t * a.chunk;
@@ -599,8 +640,17 @@ __global__ void twiddle_gen_kernel(uint32_t *table, int64_t count, const __grid_
   const int64_t e1 = (e0 + a.chunk < count) ? e0 + a.chunk : count;
   for (int64_t e = e0; e < e1; ++e) {
     uint32_t wp[K];
-    if constexpr (MONT) zero_n<K>(wp); else shoup_companion_dev<K>(wp, x, a.F.q);
-    stg_elem<K>(table + e * (2 * K), x);
+    if constexpr (MONT && PLAIN) {  // Montgomery-domain powers stored plain with their Shoup companion
+      uint32_t one[K], w[K];
+      zero_n<K>(one);
+      one[0] = 1u;
+      mont_mul<K>(w, x, one, a.F.q, a.F.qinv);
+      shoup_companion_dev<K>(wp, w, a.F.q);
+      stg_elem<K>(table + e * (2 * K), w);
+    } else {
+      if constexpr (MONT) zero_n<K>(wp); else shoup_companion_dev<K>(wp, x, a.F.q);
+      stg_elem<K>(table + e * (2 * K), x);
+    }
     stg_elem<K>(table + e * (2 * K) + K, wp);
     uint32_t r[K];
     tw_mul<K, MONT>(r, x, a.base, a.F);
@@ -629,7 +679,8 @@ __global__ void twiddle_extract_kernel(const uint32_t *table, int64_t count, uin
 // ------------------------------------------------------------------ host side
 
 template <int K>
-static int gen_table(const wm_field *f, uint32_t *table, int64_t count, const Big &base, const Big &scale) {
+static int gen_table(const wm_field *f, uint32_t *table, int64_t count, const Big &base, const Big &scale,
+                     int mode) {
   TwGenArgs<K> a;
   a.F = field_const<K>(f);
   const Big bm = f->mont ? to_mont(base, f->q) : base, sm = f->mont ? to_mont(scale, f->q) : scale;
@@ -642,7 +693,10 @@ static int gen_table(const wm_field *f, uint32_t *table, int64_t count, const Bi
   int grid = (int)((threads + 127) / 128);
   if constexpr (mont_ntt_built<K>()) {
     if (f->mont) {
-      twiddle_gen_kernel<K, true><<<grid, 128>>>(table, count, a);
+      if (mode == 2)
+        twiddle_gen_kernel<K, true, true><<<grid, 128>>>(table, count, a);
+      else
+        twiddle_gen_kernel<K, true><<<grid, 128>>>(table, count, a);
       WM_LAUNCH_CHECK("twiddle_gen launch");
       return WM_OK;
     }
@@ -663,7 +717,7 @@ static NttConst<K> ntt_const(const wm_ntt_plan *pl) {
     c.p3[j] = pl->p3[j];
     c.p4[j] = pl->p4[j];
     c.np[j] = pl->np[j];
-    c.sc[j] = pl->field->mont ? pl->ninv_mont[j] : pl->ninv[j];
+    c.sc[j] = pl->mode == 1 ? pl->ninv_mont[j] : pl->ninv[j];
     c.scp[j] = pl->ninv_sh[j];
   }
   return c;
@@ -679,13 +733,13 @@ static size_t pass_smem(int K, const wm_pass_plan &ps) {
   return round4_h((size_t)ps.G * L * K) * sizeof(uint32_t) + twimg_bytes(K, ps.logL) + 16;  // + mbarrier
 }
 
-template <int K, bool MONT>
+template <int K, int MODE>
 static int run_passes_t(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
                         uint32_t *ws, cudaStream_t st, int only_pass, const uint32_t *mul_by) {
   static std::atomic<uint64_t> attr_done{0};
   if (first_on_device(attr_done)) {
-    WM_CUDA_TRY(cudaFuncSetAttribute(ntt_col_pass<K, MONT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    WM_CUDA_TRY(cudaFuncSetAttribute(ntt_row_pass<K, MONT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    WM_CUDA_TRY(cudaFuncSetAttribute(ntt_col_pass<K, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    WM_CUDA_TRY(cudaFuncSetAttribute(ntt_row_pass<K, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
   }
   const NttConst<K> c = ntt_const<K>(pl);
   for (int pi = 0; pi < (int)pl->passes.size(); ++pi) {
@@ -727,12 +781,12 @@ static int run_passes_t(const wm_ntt_plan *pl, bool inverse, const uint32_t *in,
     if (ps.column) {
       const uint32_t *tw_out = inverse ? (ps.scaled_table ? pl->tw_inv_scaled : pl->tw_inv) : pl->tw_fwd;
       dim3 grid((unsigned)(ps.lines_outer * (ps.lines_inner / ps.G)), (unsigned)batch);
-      ntt_col_pass<K, MONT><<<grid, 256, smem, st>>>(src, dst, tw_out, d, c);
+      ntt_col_pass<K, MODE><<<grid, 256, smem, st>>>(src, dst, tw_out, d, c);
       WM_LAUNCH_CHECK("ntt_col_pass launch");
     } else {
       const int64_t lines = batch * ps.lines_inner;
       dim3 grid((unsigned)((lines + ps.G - 1) / ps.G));
-      ntt_row_pass<K, MONT><<<grid, 256, smem, st>>>(src, dst, d, c);
+      ntt_row_pass<K, MODE><<<grid, 256, smem, st>>>(src, dst, d, c);
       WM_LAUNCH_CHECK("ntt_row_pass launch");
     }
   }
@@ -743,10 +797,11 @@ template <int K>
 static int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
                       uint32_t *ws, cudaStream_t st, int only_pass = -1, const uint32_t *mul_by = nullptr) {
   if constexpr (mont_ntt_built<K>()) {
-    if (pl->field->mont) return run_passes_t<K, true>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);
+    if (pl->mode == 1) return run_passes_t<K, 1>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);
+    if (pl->mode == 2) return run_passes_t<K, 2>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);
   }
-  if (pl->field->mont) return fail(WM_EUNSUPPORTED, "limb count not built into the full-width NTT kernels");
-  return run_passes_t<K, false>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);
+  if (pl->mode != 0) return fail(WM_EUNSUPPORTED, "limb count not built into the full-width NTT kernels");
+  return run_passes_t<K, 0>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);
 }
 
 static int plan_passes(wm_ntt_plan *pl) {
@@ -880,13 +935,13 @@ static int create_tables(wm_ntt_plan *pl, const Big &root, const Big &root_inv) 
   WM_CUDA_TRY(cudaMalloc(&pl->tw_inv, bytes));
   Big one(K, 0u);
   one[0] = 1;
-  int rc = gen_table<K>(pl->field, pl->tw_fwd, n, root, one);
+  int rc = gen_table<K>(pl->field, pl->tw_fwd, n, root, one, pl->mode);
   if (rc) return rc;
-  rc = gen_table<K>(pl->field, pl->tw_inv, n, root_inv, one);
+  rc = gen_table<K>(pl->field, pl->tw_inv, n, root_inv, one, pl->mode);
   if (rc) return rc;
   if (pl->passes.size() > 1) {
     WM_CUDA_TRY(cudaMalloc(&pl->tw_inv_scaled, bytes));
-    rc = gen_table<K>(pl->field, pl->tw_inv_scaled, n, root_inv, pl->ninv);
+    rc = gen_table<K>(pl->field, pl->tw_inv_scaled, n, root_inv, pl->ninv, pl->mode);
     if (rc) return rc;
   }
   // per-pass twiddle images (forward block, then inverse block)
@@ -940,6 +995,9 @@ int wm_ntt_plan_create(const wm_field *f, int64_t n, const uint32_t *root_host, 
   Big root(root_host, root_host + K), root_inv(root_inv_host, root_inv_host + K);
   pl->ninv = Big(n_inv_host, n_inv_host + K);
   if (f->mont) pl->ninv_mont = to_mont(pl->ninv, f->q);
+  // arithmetic mode: full-width fields with two bits of headroom take the
+  // Shoup / [0, 4p) path, the rest the Montgomery path (Arith<K, MODE>)
+  pl->mode = !f->mont ? 0 : (big_bitlen(f->q) <= 32 * K - 2 ? 2 : 1);
   // Shoup companion of n^-1 and np = 2^(32K) - p on the host.
   {
     Big num = big_shl(pl->ninv, 32 * K, 2 * K);
@@ -1111,7 +1169,7 @@ int wm_ntt_twiddles(const wm_ntt_plan *p, int inverse, int64_t count, uint32_t *
 #define WM_CASE(k)                                                                             \
   case k:                                                                                      \
     if constexpr (mont_ntt_built<k>()) {                                                       \
-      if (p->field->mont) {                                                                    \
+      if (p->mode == 1) {                                                                      \
         twiddle_extract_kernel<k, true><<<grid, 256, 0, (cudaStream_t)stream>>>(              \
             table, count, out, field_const<k>(p->field));                                      \
         break;                                                                                 \

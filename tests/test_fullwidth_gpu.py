@@ -114,16 +114,19 @@ _PRIMES: dict = {}
 
 
 def _prime(name: str, bits: int) -> int:
-    """Named curve/FHE primes, or a random full-width 2^24-NTT prime (cached)."""
+    """Named curve/FHE primes, or a random 2^24-NTT prime of full width
+    ("random") or two bits below it ("random2": the NTT's Shoup / [0, 4p)
+    mode for full-width fields) (cached)."""
     if name in _NAMED:
         return _NAMED[name]
     if (name, bits) not in _PRIMES:
-        _PRIMES[(name, bits)] = _ntt_prime(bits, 24, bits)
+        _PRIMES[(name, bits)] = _ntt_prime(bits - (2 if name == "random2" else 0), 24, bits)
     return _PRIMES[(name, bits)]
 
 
 FIELDS = [(256, "bls12_381_r"), (256, "bn254_r"), (64, "goldilocks")] + [
-    (bits, "random") for bits in (32, 128, 384, 512, 768, 1024)]
+    (bits, "random") for bits in (32, 128, 384, 512, 768, 1024)] + [
+    (bits, "random2") for bits in (64, 128, 384, 768, 1024)]
 
 
 @pytest.mark.parametrize("bits,name", FIELDS)
@@ -152,7 +155,8 @@ def test_ntt_full_width_vs_exact_oracle(cuda, bits, name, logn):
 
 
 @pytest.mark.parametrize("bits,name,logn", [(256, "bls12_381_r", 16), (256, "bls12_381_r", 21),
-                                             (64, "goldilocks", 22), (1024, "random", 19)])
+                                             (64, "goldilocks", 22), (1024, "random", 19),
+                                             (256, "bn254_r", 21), (768, "random2", 20)])
 def test_ntt_full_width_large(cuda, bits, name, logn):
     """Multi-pass plans: INTT(NTT(x)) == x and Horner evaluations of outputs."""
     import torch

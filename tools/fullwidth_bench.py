@@ -36,6 +36,12 @@ def main():
     ms = t(lambda: (plan.forward(x, out=y, workspace=ws), plan.inverse(y, out=z, workspace=ws)))
     assert torch.equal(z, x)
     out["bls12_381_r_ntt_2p16_us_per_transform"] = round(ms * 1e3 / (2 * B), 3)
+    BN = 21888242871839275222246405745257275088548364400416034343698204186575808495617
+    fb = dev.Field(256, BN, "montgomery")
+    pb = dev.NttPlan(fb, params(BN, n))
+    msb = t(lambda: (pb.forward(x, out=y, workspace=ws), pb.inverse(y, out=z, workspace=ws)))
+    assert torch.equal(z, x)
+    out["bn254_r_ntt_2p16_us_per_transform"] = round(msb * 1e3 / (2 * B), 3)
     ref = K.get_plan(256, find_ntt_params(256, n))
     ms2 = t(lambda: (ref.forward(x, out=y, workspace=ws), ref.inverse(y, out=z, workspace=ws)))
     out["reference_range_ntt_2p16_us_per_transform"] = round(ms2 * 1e3 / (2 * B), 3)
