@@ -257,3 +257,30 @@ def test_host_pipeline_ramped_chunks(cuda):
     torch.cuda.synchronize()
     want = plan.field.to_ref_layout(plan.forward(x), 64, 4).cpu()
     assert torch.equal(buf, want)
+
+
+def test_host_pipeline_repeated_calls(cuda):
+    """Repeated wm_ntt_host calls on the same buffers with new data and
+    changing shapes (the slot pool grows and is reused) stay exact."""
+    dev = _dev()
+    import torch
+    n = 1 << 12
+    plan = plan_for(256, n)
+    f = plan.field
+    for batch, chunk in ((9, 0), (9, 0), (9, 2), (9, 0), (5, 0)):
+        g = torch.Generator(device="cuda").manual_seed(batch * 10 + chunk)
+        x = torch.randint(-(1 << 31), 1 << 31, (batch * n, 8), dtype=torch.int32, device="cuda", generator=g)
+        x[:, 7] &= (1 << 27) - 1
+        want = f.to_ref_layout(plan.forward(x), 64, 4).cpu()
+        for _ in range(3):
+            host_in = getattr(test_host_pipeline_repeated_calls, "_hin", None)
+            if host_in is None or host_in.shape[0] != batch * n:
+                host_in = torch.empty((batch * n, 4), dtype=torch.int64).pin_memory()
+                host_out = torch.empty_like(host_in).pin_memory()
+                test_host_pipeline_repeated_calls._hin, test_host_pipeline_repeated_calls._hout = host_in, host_out
+            host_out = test_host_pipeline_repeated_calls._hout
+            host_in.copy_(f.to_ref_layout(x, 64, 4).cpu())
+            host_out.zero_()
+            plan.host_transform(host_in, host_out, mode="forward", word_bits=64, ref_words=4, chunk=chunk)
+            torch.cuda.synchronize()
+            assert torch.equal(host_out, want), (batch, chunk)
