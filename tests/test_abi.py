@@ -71,3 +71,32 @@ def test_field_create_validation(lib):
     big = (ctypes.c_uint32 * 1)(0xFFFFFFFF)
     assert lib.wm_field_create(32, big, 1, ctypes.byref(h)) == _lib.WM_EINVAL
     assert lib.wm_field_create(4000, one, 1, ctypes.byref(h)) == _lib.WM_EUNSUPPORTED
+
+
+def _limbs(v: int, k: int):
+    return (ctypes.c_uint32 * k)(*[(v >> (32 * i)) & 0xFFFFFFFF for i in range(k)])
+
+
+def test_full_width_and_padded_field_creation(lib):
+    """Host-side field setup (no device work): full-width (Montgomery)
+    fields, their validation, and widths padded to a built limb count."""
+    h = ctypes.c_void_p()
+    b, k, s = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    secp = 2**256 - 2**32 - 977
+    assert lib.wm_field_create_ex(256, _limbs(secp, 8), 8, _lib.WM_FIELD_MONTGOMERY, ctypes.byref(h)) == 0
+    assert lib.wm_field_info(h, ctypes.byref(b), ctypes.byref(k), ctypes.byref(s)) == 0
+    assert (b.value, k.value, s.value) == (256, 8, 0)  # top bit set: full-width Barrett shift 0
+    lib.wm_field_destroy(h)
+    # the Barrett path keeps the reference range
+    assert lib.wm_field_create_ex(256, _limbs(secp, 8), 8, 0, ctypes.byref(h)) == _lib.WM_EINVAL
+    # Montgomery needs an odd modulus; Karatsuba applies to Barrett fields only
+    assert lib.wm_field_create_ex(256, _limbs(secp + 1, 8), 8, _lib.WM_FIELD_MONTGOMERY, ctypes.byref(h)) == _lib.WM_EINVAL
+    assert lib.wm_field_create_ex(256, _limbs(secp, 8), 8, 3, ctypes.byref(h)) == _lib.WM_EINVAL
+    # 640 bits (20 limbs, no kernels of its own) runs zero-padded to 24 limbs
+    assert lib.wm_limbs_for_bits(640) == 24 and lib.wm_limbs_for_bits(512) == 16
+    q640 = 2**636 - 3 * 2**400 - 1  # odd, reference range
+    assert lib.wm_field_create_ex(640, _limbs(q640, 20), 20, 0, ctypes.byref(h)) == 0
+    assert lib.wm_field_info(h, ctypes.byref(b), ctypes.byref(k), ctypes.byref(s)) == 0
+    assert k.value == 24
+    lib.wm_field_destroy(h)
+    assert lib.wm_field_create_ex(640, _limbs(q640 + 1, 20), 20, 0, ctypes.byref(h)) == _lib.WM_EUNSUPPORTED
