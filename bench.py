@@ -165,6 +165,12 @@ def peaks():
         return {}
 
 
+def _alg_wmul(n: int) -> float:
+    """SURVEY §8(d) algorithmic work of one forward 256-bit transform:
+    (n/2) log2 n butterflies x 3k^2 word products."""
+    return (n // 2) * (n.bit_length() - 1) * ALG_WMUL_PER_BFLY
+
+
 def int_peak_wmul_per_s(sm_mhz: float | None):
     """Integer-pipe roofline: 32 IMAD.WIDE (32x32->64 word products) per clock
     per SM (measured half-rate, profiles/r01_imad_rate.jsonl) x 148 SMs."""
@@ -450,6 +456,8 @@ def run_four_step(args, torch, rank, world, pg):
         e1.record(stream)
         torch.cuda.synchronize()
         res["single_gpu_plan_ms_per_forward"] = round(e0.elapsed_time(e1) / reps, 4)
+        res["single_gpu_plan_int_roofline_frac"] = round(
+            _alg_wmul(n) / (e0.elapsed_time(e1) / reps * 1e-3) / int_peak_wmul_per_s(None)[0], 3)
         res["single_gpu_plan_passes"] = plan.pass_log_sizes
         del xs, ys, ws
     torch.cuda.empty_cache()
@@ -606,6 +614,9 @@ def run_batched_2p20(args, torch, rank, world, pg):
     torch.cuda.empty_cache()
     return {"n": n, "batch_total": total, "ranks": world, "ms_fwd_plus_inv": round(ms, 3),
             "us_per_transform": round(ms * 1e3 / (2 * total), 2), "passes": plan.pass_log_sizes,
+            "int_roofline_frac": round(_alg_wmul(n) * 2 * (total // world) / (ms * 1e-3) / int_peak_wmul_per_s(None)[0], 3),
+            "int_roofline_basis": "reference algorithmic work (3k^2 products per butterfly) / time / per-GPU integer "
+                                  "peak; above 1 because Shoup + lazy reduction execute ~0.5 of those products",
             "scaling": "strong (fixed total batch 256)", "note": "max over ranks; inputs 8 GiB / world per rank"}
 
 
