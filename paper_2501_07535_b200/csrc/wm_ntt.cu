@@ -43,7 +43,7 @@
 #define WM_NTT_MINB 2
 #endif
 #ifndef WM_NTT_MINB_SMALL  // K <= 4 (<= 128-bit): lighter register footprint
-#define WM_NTT_MINB_SMALL 2
+#define WM_NTT_MINB_SMALL 4
 #endif
 #ifndef WM_NTT_MINB_WIDE  // K > 12: 2 CTAs/SM with a few spilled registers beat
 #define WM_NTT_MINB_WIDE 2   // 1 CTA/SM (profiles/r01_ab_wide_occupancy.txt: 768-bit 102 -> 91 us)
@@ -57,6 +57,9 @@
                           : (K) <= 12        ? WM_NTT_MINB                                        \
                                              : WM_NTT_MINB_WIDE))
 // Target tile size (32-bit words of data per CTA; 16384 = 64 KB).
+#ifndef WM_NTT_TILE_WORDS_SMALL  // K <= 4: 32 KB tiles, 4 CTAs/SM (128-bit 2^16: 3.60 -> 3.46 us,
+#define WM_NTT_TILE_WORDS_SMALL 8192  // 64-bit 3.19 -> 2.57 us; profiles/r01_ab_small_tiles.txt)
+#endif
 #ifndef WM_NTT_TILE_WORDS
 #define WM_NTT_TILE_WORDS 16384
 #endif
@@ -816,7 +819,8 @@ static int plan_passes(wm_ntt_plan *pl) {
   for (int i = 0; i < logn % P; ++i) sizes[i] += 1;
   auto choose_G = [&](int logL, int64_t inner_cap) {
     int64_t words_line = ((int64_t)1 << logL) * K;
-    int64_t G = std::max<int64_t>(1, WM_NTT_TILE_WORDS / words_line);  // data words per CTA
+    const int64_t tile = K <= 4 ? WM_NTT_TILE_WORDS_SMALL : WM_NTT_TILE_WORDS;  // data words per CTA
+    int64_t G = std::max<int64_t>(1, tile / words_line);
     G = std::min<int64_t>(G, 32);
     int64_t g = 1;
     while (g * 2 <= G) g *= 2;
