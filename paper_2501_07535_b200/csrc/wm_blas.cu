@@ -411,7 +411,15 @@ int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags,
   if (flags & ~(WM_FIELD_KARATSUBA | WM_FIELD_MONTGOMERY)) return fail(WM_EINVAL, "unknown field flags");
   if (flags & WM_FIELD_MONTGOMERY) {
     if (flags & WM_FIELD_KARATSUBA) return fail(WM_EINVAL, "Karatsuba applies to Barrett fields only");
-    if (!mont_supports(K)) return fail(WM_EUNSUPPORTED, "width not built into the full-width (Montgomery) kernels");
+    if (!mont_supports(K)) {  // zero-pad to the next limb count with Montgomery kernels
+      int Kp = -1;
+#define WM_CASE(k) if (k >= K && (Kp < 0 || k < Kp)) Kp = k;
+      WM_MONT_KS(WM_CASE)
+#undef WM_CASE
+      if (Kp < 0) return fail(WM_EUNSUPPORTED, "width not built into the full-width (Montgomery) kernels");
+      K = Kp;
+      q = big_resize(q, K);
+    }
     if (!(q[0] & 1u)) return fail(WM_EINVAL, "full-width (Montgomery) fields need an odd modulus");
     if (qb > bits) return fail(WM_EINVAL, "modulus wider than the field width");
     if (qb < 3) return fail(WM_EINVAL, "modulus must exceed 2");

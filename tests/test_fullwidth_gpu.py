@@ -25,6 +25,8 @@ CASES = [
     (768, 2**768 - 1), (512, 2**512 - 569),
     # moduli that leave the top limb empty (vmul takes the two-Montgomery-product path)
     (256, M127), (1024, SECP256K1_P), (64, 2**32 - 5),
+    # limb counts without Montgomery kernels of their own (zero-padded to 4 / 8 / 16 limbs)
+    (96, 2**96 - 17), (160, 2**160 - 47), (480, 2**480 - 65),
 ]
 
 
@@ -126,7 +128,8 @@ def _prime(name: str, bits: int) -> int:
 
 FIELDS = [(256, "bls12_381_r"), (256, "bn254_r"), (64, "goldilocks")] + [
     (bits, "random") for bits in (32, 128, 384, 512, 768, 1024)] + [
-    (bits, "random2") for bits in (64, 128, 384, 768, 1024)]
+    (bits, "random2") for bits in (64, 128, 384, 768, 1024)] + [
+    (96, "random"), (160, "random"), (224, "random2")]  # limb counts padded to a Montgomery build
 
 
 @pytest.mark.parametrize("bits,name", FIELDS)
