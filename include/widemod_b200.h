@@ -84,7 +84,10 @@ int wm_field_create(int bits, const uint32_t *q_host, int q_limbs, wm_field **ou
  * e.g. secp256k1's p or BLS12-381's r at 256 bits).  Sums carry-aware,
  * products by Montgomery multiplication (vmul: two Montgomery products, axpy:
  * one with the scalar in Montgomery form); inputs and outputs stay canonical
- * residues.  Built for 1, 2, 4, 8, 12, 16, 24 and 32 limbs. */
+ * residues.  Kernels for 1, 2, 4, 8, 12, 16, 24 and 32 limbs; other widths run
+ * zero-padded to the next of those (wm_field_info reports the storage limbs).
+ * A width whose limb count has no Barrett kernels either (513-736, 769-992
+ * bits) is created as such a padded Montgomery field when q is odd. */
 #define WM_FIELD_MONTGOMERY 2
 int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags, wm_field **out);
 int wm_field_destroy(wm_field *f);
