@@ -20,7 +20,8 @@ while time.time() < t_end:
     bits = rnd.choice(widths)
     try:
         if kind == "ntt":
-            logn = rnd.randint(1, 14 if bits <= 512 else 11)
+            big = len(sys.argv) > 3 and sys.argv[3] == "big"
+            logn = rnd.randint(1, (18 if big else 14) if bits <= 256 else (14 if bits <= 512 else 11))
             n = 1 << logn
             try:
                 prm = find_ntt_params(bits, n)
