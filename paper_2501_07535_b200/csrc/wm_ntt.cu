@@ -42,6 +42,9 @@
 #ifndef WM_NTT_MINB
 #define WM_NTT_MINB 2
 #endif
+#ifndef WM_NTT_THREADS  // threads per pass CTA
+#define WM_NTT_THREADS 256
+#endif
 #ifndef WM_NTT_MINB_SMALL  // K <= 4 (<= 128-bit): lighter register footprint
 #define WM_NTT_MINB_SMALL 4
 #endif
@@ -52,7 +55,7 @@
 #define WM_NTT_MINB_MONT 2
 #endif
 #define WM_NTT_BOUNDS(K, MODE)                                                                      \
-  __launch_bounds__(256, ((MODE) == 1 && (K) <= 8 ? WM_NTT_MINB_MONT                              \
+  __launch_bounds__(WM_NTT_THREADS, ((MODE) == 1 && (K) <= 8 ? WM_NTT_MINB_MONT                   \
                           : (K) <= 4         ? WM_NTT_MINB_SMALL                                  \
                           : (K) <= 12        ? WM_NTT_MINB                                        \
                                              : WM_NTT_MINB_WIDE))
@@ -784,12 +787,12 @@ static int run_passes_t(const wm_ntt_plan *pl, bool inverse, const uint32_t *in,
     if (ps.column) {
       const uint32_t *tw_out = inverse ? (ps.scaled_table ? pl->tw_inv_scaled : pl->tw_inv) : pl->tw_fwd;
       dim3 grid((unsigned)(ps.lines_outer * (ps.lines_inner / ps.G)), (unsigned)batch);
-      ntt_col_pass<K, MODE><<<grid, 256, smem, st>>>(src, dst, tw_out, d, c);
+      ntt_col_pass<K, MODE><<<grid, WM_NTT_THREADS, smem, st>>>(src, dst, tw_out, d, c);
       WM_LAUNCH_CHECK("ntt_col_pass launch");
     } else {
       const int64_t lines = batch * ps.lines_inner;
       dim3 grid((unsigned)((lines + ps.G - 1) / ps.G));
-      ntt_row_pass<K, MODE><<<grid, 256, smem, st>>>(src, dst, d, c);
+      ntt_row_pass<K, MODE><<<grid, WM_NTT_THREADS, smem, st>>>(src, dst, d, c);
       WM_LAUNCH_CHECK("ntt_row_pass launch");
     }
   }
