@@ -169,40 +169,67 @@ constexpr int kMontField = 2;
 #endif
 
 template <int K, int OP, int STRAT>
-__global__ void __launch_bounds__(256, (K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? WM_BLAS_MINB_MID : 1)) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
-                                                   int64_t n, const __grid_constant__ BlasArgs<K> args) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    uint32_t x[K], y[K], r[K];
-    load_elem<K>(x, a, i);
-    load_elem<K>(y, b, i);
-    if constexpr (STRAT == kMontField) {
-      if constexpr (OP == OP_VADD) {
-        add_mod_full<K>(r, x, y, args.F.q);
-      } else if constexpr (OP == OP_VSUB) {
-        sub_mod<K>(r, x, y, args.F.q);
-      } else if constexpr (OP == OP_VMUL) {
-        if (args.F.s <= 31) {
-          mul_barrett_full<K>(r, x, y, args.F);
-        } else {
-          mul_mont_plain<K>(r, x, y, args.F);
-        }
-      } else {  // scal = a R mod q: one Montgomery product gives a x
-        uint32_t t[K];
-        mont_mul<K>(t, args.scal, x, args.F.q, args.F.qinv);
-        add_mod_full<K>(r, t, y, args.F.q);
-      }
-    } else if constexpr (OP == OP_VADD) {
-      add_mod<K>(r, x, y, args.F.q);
+WM_DEV void blas_elem(uint32_t (&r)[K], const uint32_t (&x)[K], const uint32_t (&y)[K], const BlasArgs<K> &args) {
+  if constexpr (STRAT == kMontField) {
+    if constexpr (OP == OP_VADD) {
+      add_mod_full<K>(r, x, y, args.F.q);
     } else if constexpr (OP == OP_VSUB) {
       sub_mod<K>(r, x, y, args.F.q);
     } else if constexpr (OP == OP_VMUL) {
-      mul_barrett<K, STRAT>(r, x, y, args.F);
-    } else {
+      if (args.F.s <= 31) {
+        mul_barrett_full<K>(r, x, y, args.F);
+      } else {
+        mul_mont_plain<K>(r, x, y, args.F);
+      }
+    } else {  // scal = a R mod q: one Montgomery product gives a x
       uint32_t t[K];
-      mul_barrett_pre<K, barrett_style<K>(), STRAT>(t, args.scal, x, args.F);
-      add_mod<K>(r, t, y, args.F.q);
+      mont_mul<K>(t, args.scal, x, args.F.q, args.F.qinv);
+      add_mod_full<K>(r, t, y, args.F.q);
     }
+  } else if constexpr (OP == OP_VADD) {
+    add_mod<K>(r, x, y, args.F.q);
+  } else if constexpr (OP == OP_VSUB) {
+    sub_mod<K>(r, x, y, args.F.q);
+  } else if constexpr (OP == OP_VMUL) {
+    mul_barrett<K, STRAT>(r, x, y, args.F);
+  } else {
+    uint32_t t[K];
+    mul_barrett_pre<K, barrett_style<K>(), STRAT>(t, args.scal, x, args.F);
+    add_mod<K>(r, t, y, args.F.q);
+  }
+}
+
+// Elements per thread per grid-stride step for small limb counts (loads of
+// E elements in flight before their arithmetic).
+#ifndef WM_BLAS_EPT_SMALL
+#define WM_BLAS_EPT_SMALL 1
+#endif
+
+template <int K, int OP, int STRAT>
+__global__ void __launch_bounds__(256, (K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? WM_BLAS_MINB_MID : 1)) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
+                                                   int64_t n, const __grid_constant__ BlasArgs<K> args) {
+  constexpr int E = K <= 4 ? WM_BLAS_EPT_SMALL : 1;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if constexpr (E > 1) {
+    for (; i + (E - 1) * stride < n; i += E * stride) {
+      uint32_t x[E][K], y[E][K], r[E][K];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        load_elem<K>(x[e], a, i + e * stride);
+        load_elem<K>(y[e], b, i + e * stride);
+      }
+#pragma unroll
+      for (int e = 0; e < E; ++e) blas_elem<K, OP, STRAT>(r[e], x[e], y[e], args);
+#pragma unroll
+      for (int e = 0; e < E; ++e) store_elem<K>(out, i + e * stride, r[e]);
+    }
+  }
+  for (; i < n; i += stride) {
+    uint32_t x[K], y[K], r[K];
+    load_elem<K>(x, a, i);
+    load_elem<K>(y, b, i);
+    blas_elem<K, OP, STRAT>(r, x, y, args);
     store_elem<K>(out, i, r);
   }
 }
