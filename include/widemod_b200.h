@@ -29,9 +29,13 @@
  *   - Every function returns WM_OK (0) or a nonzero status; wm_last_error()
  *     returns a thread-local message for the last failure on this thread.
  *   - Plans/fields are immutable after creation and may be shared between
- *     threads; calls on different streams may run concurrently, except that
- *     one NTT plan's internal workspace (used when workspace == NULL) is
- *     serialised by a mutex.
+ *     threads; calls on different streams may run concurrently.  One NTT
+ *     plan's internal workspace (used when workspace == NULL) is shared by
+ *     all its callers: those calls are stream-ordered one after another (each
+ *     waits on the device for the previous user, on whatever stream), so pass
+ *     a workspace per stream for concurrent multi-pass transforms.
+ *   - Setup calls (field/plan creation) never synchronise the device or the
+ *     legacy default stream: plan tables are generated on a private stream.
  */
 #ifndef WIDEMOD_B200_H
 #define WIDEMOD_B200_H
@@ -151,7 +155,9 @@ int wm_ntt_inverse(const wm_ntt_plan *p, const uint32_t *in, uint32_t *out, int6
  * out = INTT(NTT(a) * NTT(b)) — the reference's own convolution check
  * (verify.py:195-223: run_ntt, run_vector(vmul), run_ntt(intt)) as three
  * launch sequences, with the pointwise product fused into the epilogue of
- * the forward transform of b.  a may alias out; b may not. */
+ * the forward transform of b.  a may alias out; b may not.  Three-pass plans
+ * hold NTT(a) in a stream-ordered temporary (cudaMallocAsync) of
+ * batch * n * K words. */
 int wm_ntt_convolve(const wm_ntt_plan *p, const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t batch,
                     void *workspace, void *stream);
 

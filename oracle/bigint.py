@@ -237,3 +237,31 @@ def uniform_residues(rng: np.random.Generator, count: int, q: int) -> list[int]:
             if v < q:
                 out.append(v)
     return out
+
+
+def uniform_residue_limbs(rng: np.random.Generator, count: int, q: int, limbs: int | None = None) -> np.ndarray:
+    """uniform_residues as a uint32 limb array [count, limbs] (little-endian
+    limbs), vectorised: the same draws, the same rejections, the same order
+    (pinned equal in tests/test_oracle_pinned.py).  For the full-size parity
+    fixtures (2^16 x 64 .. 2^24 elements) where Python ints are too slow."""
+    k = (q.bit_length() + 31) // 32
+    top_bits = q.bit_length() - 32 * (k - 1)
+    qw = [(q >> (32 * j)) & 0xFFFFFFFF for j in range(k)]
+    parts = []
+    have = 0
+    while have < count:
+        need = count - have
+        l = rng.integers(0, 1 << 32, size=(need, k), dtype=np.uint64).astype("<u4")
+        l[:, -1] &= np.uint32((1 << top_bits) - 1)
+        gt = np.zeros(need, dtype=bool)
+        eq = np.ones(need, dtype=bool)
+        for j in range(k - 1, -1, -1):
+            gt |= eq & (l[:, j] > qw[j])
+            eq &= l[:, j] == qw[j]
+        keep = l[~(gt | eq)]
+        parts.append(keep)
+        have += keep.shape[0]
+    out = np.concatenate(parts)[:count]
+    if limbs is not None and limbs > k:
+        out = np.concatenate([out, np.zeros((count, limbs - k), dtype="<u4")], axis=1)
+    return np.ascontiguousarray(out)

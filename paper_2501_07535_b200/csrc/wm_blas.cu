@@ -237,16 +237,20 @@ __global__ void __launch_bounds__(256, (K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? W
 template <int K, int OP, int STRAT>
 static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, uint32_t *out,
                        int64_t n, const uint32_t *scal_host, cudaStream_t st) {
-  static int blocks_per_sm = -1;
-  static int sm_count = 0;
-  if (blocks_per_sm < 0) {
-    int dev;
-    WM_CUDA_TRY(cudaGetDevice(&dev));
-    WM_CUDA_TRY(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
-    int nb = 0;
+  // resident CTAs per SM and SM count of the current device, cached per
+  // (kernel, device): packed as blocks * 4096 + SMs, 0 = not yet known
+  static std::atomic<int> occ[64];
+  int dev = 0;
+  WM_CUDA_TRY(cudaGetDevice(&dev));
+  int packed = occ[dev & 63].load(std::memory_order_relaxed);
+  if (packed == 0) {
+    int sms = 0, nb = 0;
+    WM_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     WM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, blas_kernel<K, OP, STRAT>, 256, 0));
-    blocks_per_sm = std::max(1, nb);
+    packed = std::max(1, nb) * 4096 + sms;
+    occ[dev & 63].store(packed, std::memory_order_relaxed);
   }
+  const int blocks_per_sm = packed / 4096, sm_count = packed % 4096;
   BlasArgs<K> args;
   args.F = field_const<K>(f);
   for (int j = 0; j < K; ++j) args.scal[j] = 0;
@@ -269,6 +273,10 @@ static int blas_dispatch(int op, const wm_field *f, const uint32_t *a, const uin
   if (n < 0) return fail(WM_EINVAL, "negative length");
   if (n == 0) return WM_OK;
   if (!a || !b || !out) return fail(WM_EINVAL, "null data pointer");
+  if (scal_host) {  // the axpy scalar must be a canonical residue, like every input
+    const Big sc(scal_host, scal_host + f->K);
+    if (big_ge(sc, f->q)) return fail(WM_EINVAL, "axpy scalar must be below the modulus");
+  }
   cudaStream_t st = (cudaStream_t)stream;
   if (f->mont) {
     switch (f->K) {
@@ -486,6 +494,13 @@ int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags,
     return WM_OK;
   }
   if (qb > M) return fail(WM_EINVAL, "modulus must be below 2^(32K-4)");
+  {
+    // a power of two normalises to qn = 2^(M-1), whose Barrett constant
+    // 8 floor(2^(2M) / qn) = 2^(32K) does not fit K limbs
+    int ones = 0;
+    for (int j = 0; j < K; ++j) ones += __builtin_popcount(q[j]);
+    if (ones == 1) return fail(WM_EINVAL, "power-of-two modulus not supported by the Barrett kernels");
+  }
   if (M - qb > 31) return fail(WM_EINVAL, "modulus too small for the field width (normalisation shift > 31)");
   wm_field *f = new wm_field();
   f->karatsuba = (flags & WM_FIELD_KARATSUBA) != 0;

@@ -30,44 +30,53 @@ constexpr int TT = 32;  // tile edge (elements)
 // elements staged in shared memory word-by-word (W words per element,
 // padded row stride to dodge bank conflicts).
 __global__ void __launch_bounds__(256) transpose_words_kernel(const uint32_t *in, uint32_t *out, int W,
-                                                              int64_t rows, int64_t cols) {
+                                                              int64_t rows, int64_t cols, int64_t batch) {
   extern __shared__ uint32_t tile[];  // TT * (TT*W + 1) words
-  const int64_t b = blockIdx.z;
-  const int64_t r0 = (int64_t)blockIdx.y * TT, c0 = (int64_t)blockIdx.x * TT;
+  const int64_t c0 = (int64_t)blockIdx.x * TT;
   const int64_t plane = rows * cols * W;
-  const uint32_t *src = in + b * plane;
-  uint32_t *dst = out + b * plane;
   const int stride = TT * W + 1;
-  // load: rows r0..r0+TT, each row a contiguous run of TT*W words
-  for (int idx = threadIdx.x; idx < TT * TT * W; idx += blockDim.x) {
-    const int rr = idx / (TT * W), w = idx - rr * (TT * W);
-    const int64_t r = r0 + rr, c = c0 + w / W;
-    if (r < rows && c < cols) tile[rr * stride + w] = src[(r * cols + c0) * W + w];
-  }
-  __syncthreads();
-  // store: out rows c0..c0+TT, each a contiguous run of TT*W words (elements r0..)
-  for (int idx = threadIdx.x; idx < TT * TT * W; idx += blockDim.x) {
-    const int cc = idx / (TT * W), w = idx - cc * (TT * W);
-    const int rr = w / W, ww = w - rr * W;
-    const int64_t c = c0 + cc, r = r0 + rr;
-    if (r < rows && c < cols) dst[(c * rows + r0) * W + w] = tile[rr * stride + cc * W + ww];
+  // grid-stride over row tiles (y) and transforms (z): any rows / batch
+  for (int64_t b = blockIdx.z; b < batch; b += gridDim.z) {
+    const uint32_t *src = in + b * plane;
+    uint32_t *dst = out + b * plane;
+    for (int64_t r0 = (int64_t)blockIdx.y * TT; r0 < rows; r0 += (int64_t)gridDim.y * TT) {
+      // load: rows r0..r0+TT, each row a contiguous run of TT*W words
+      for (int idx = threadIdx.x; idx < TT * TT * W; idx += blockDim.x) {
+        const int rr = idx / (TT * W), w = idx - rr * (TT * W);
+        const int64_t r = r0 + rr, c = c0 + w / W;
+        if (r < rows && c < cols) tile[rr * stride + w] = src[(r * cols + c0) * W + w];
+      }
+      __syncthreads();
+      // store: out rows c0..c0+TT, each a contiguous run of TT*W words (elements r0..)
+      for (int idx = threadIdx.x; idx < TT * TT * W; idx += blockDim.x) {
+        const int cc = idx / (TT * W), w = idx - cc * (TT * W);
+        const int rr = w / W, ww = w - rr * W;
+        const int64_t c = c0 + cc, r = r0 + rr;
+        if (r < rows && c < cols) dst[(c * rows + r0) * W + w] = tile[rr * stride + cc * W + ww];
+      }
+      __syncthreads();
+    }
   }
 }
 
 // Wide elements (>= 64 words, e.g. the N1/P-element blocks of the four-step's
 // block transpose): one CTA per element, 16-byte vector copies.
 __global__ void __launch_bounds__(256) transpose_wide_kernel(const uint32_t *in, uint32_t *out, int64_t W,
-                                                             int64_t rows, int64_t cols) {
-  const int64_t c = blockIdx.x, r = blockIdx.y, b = blockIdx.z;
+                                                             int64_t rows, int64_t cols, int64_t batch) {
+  const int64_t c = blockIdx.x;
   const int64_t plane = rows * cols * W;
-  const uint32_t *src = in + b * plane + (r * cols + c) * W;
-  uint32_t *dst = out + b * plane + (c * rows + r) * W;
-  if ((W & 3) == 0) {
-    const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
-    uint4 *d4 = reinterpret_cast<uint4 *>(dst);
-    for (int64_t i = threadIdx.x; i < W / 4; i += blockDim.x) d4[i] = __ldcs(s4 + i);
-  } else {
-    for (int64_t i = threadIdx.x; i < W; i += blockDim.x) dst[i] = src[i];
+  for (int64_t b = blockIdx.z; b < batch; b += gridDim.z) {
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+      const uint32_t *src = in + b * plane + (r * cols + c) * W;
+      uint32_t *dst = out + b * plane + (c * rows + r) * W;
+      if ((W & 3) == 0) {
+        const uint4 *s4 = reinterpret_cast<const uint4 *>(src);
+        uint4 *d4 = reinterpret_cast<uint4 *>(dst);
+        for (int64_t i = threadIdx.x; i < W / 4; i += blockDim.x) d4[i] = __ldcs(s4 + i);
+      } else {
+        for (int64_t i = threadIdx.x; i < W; i += blockDim.x) dst[i] = src[i];
+      }
+    }
   }
 }
 
@@ -260,10 +269,11 @@ int wm_transpose(int words, const uint32_t *in, uint32_t *out, int64_t rows, int
   if (words < 1 || rows < 0 || cols < 0 || batch < 0) return fail(WM_EINVAL, "bad transpose shape");
   if (rows == 0 || cols == 0 || batch == 0) return WM_OK;
   if (!in || !out || in == out) return fail(WM_EINVAL, "transpose needs distinct in/out buffers");
-  if (batch > 65535 || rows > 65535) return fail(WM_EUNSUPPORTED, "transpose batch/rows above 65535");
+  if (cols > 0x7fffffffLL * (words >= 64 ? 1 : TT)) return fail(WM_EUNSUPPORTED, "transpose cols above 2^31");
+  const unsigned gz = (unsigned)std::min<int64_t>(batch, 65535);
   if (words >= 64) {
-    dim3 g((unsigned)cols, (unsigned)rows, (unsigned)batch);
-    transpose_wide_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(in, out, words, rows, cols);
+    dim3 g((unsigned)cols, (unsigned)std::min<int64_t>(rows, 65535), gz);
+    transpose_wide_kernel<<<g, 256, 0, (cudaStream_t)stream>>>(in, out, words, rows, cols, batch);
     WM_LAUNCH_CHECK("transpose_wide launch");
     return WM_OK;
   }
@@ -272,8 +282,8 @@ int wm_transpose(int words, const uint32_t *in, uint32_t *out, int64_t rows, int
     WM_CUDA_TRY(cudaFuncSetAttribute(transpose_words_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)smem));
   }
-  dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)((rows + TT - 1) / TT), (unsigned)batch);
-  transpose_words_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(in, out, words, rows, cols);
+  dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)std::min<int64_t>((rows + TT - 1) / TT, 65535), gz);
+  transpose_words_kernel<<<grid, 256, smem, (cudaStream_t)stream>>>(in, out, words, rows, cols, batch);
   WM_LAUNCH_CHECK("transpose launch");
   return WM_OK;
 }

@@ -122,8 +122,10 @@ struct wm_ntt_plan {
   int mode = 0;        // Arith mode: 0 lazy Shoup [0,6p), 1 Montgomery, 2 Shoup [0,4p) (full-width p < 2^(32K-2))
   wm::Big ninv_mont;  // full-width fields: n^-1 R mod p (one-pass inverse scale)
   wm::Big ninv, ninv_sh, np, p2, p3, p4;  // n^-1, floor(n^-1 * 2^32K / p), 2^32K - p, 2p, 3p, 4p
-  // internal workspace (used when the caller passes none)
+  // internal workspace (used when the caller passes none): uses are
+  // stream-ordered through ws_ev (ntt_run_internal)
   std::mutex ws_mu;
+  cudaEvent_t ws_ev = nullptr;
   void *ws = nullptr;
   int64_t ws_bytes = 0;
   // host pipeline (wm_ntt_host): internal streams, events and staging slots

@@ -168,6 +168,8 @@ class Field:
             out = torch.empty_like(x)
         else:
             self._check_vec(x, out)
+        if not 0 <= int(a) < self.q:
+            raise ValueError("axpy scalar must be a canonical residue (0 <= a < q)")
         sl = _lib.u32_array(ints_to_limbs([int(a)], self.limbs)[0].tolist())
         _lib.check(self.lib.wm_axpy(self._h, sl, _ptr(x), _ptr(y), _ptr(out), n, _stream_ptr(stream)))
         return out
@@ -269,18 +271,27 @@ class NttPlan:
         """Cyclic convolution per transform: INTT(NTT(a) * NTT(b)) with the
         pointwise product fused into the forward transform of b."""
         torch = _torch()
+        K = self.limbs
+        for t in (a, b):
+            if t.dtype.itemsize != 4 or t.shape[-1] != K:
+                raise ValueError(f"expected int32 limbs [..., {self.n}, {K}]")
         if a.numel() != b.numel():
             raise ValueError("a and b differ in size")
         if out is None:
             out = torch.empty_like(a)
+        elif out.numel() != a.numel() or out.dtype.itemsize != 4:
+            raise ValueError("output size mismatch")
         if out.data_ptr() == b.data_ptr():
             raise ValueError("b may not alias out")
-        K = self.limbs
         total = a.numel() // K
         if total % self.n:
             raise ValueError(f"expected a multiple of {self.n} elements")
         batch = total // self.n
-        ws = _ptr(workspace) if workspace is not None else None
+        ws = None
+        if workspace is not None:
+            if workspace.numel() * workspace.element_size() < self.workspace_bytes(batch):
+                raise ValueError("workspace too small")
+            ws = _ptr(workspace)
         _lib.check(self.lib.wm_ntt_convolve(self._h, _ptr(a), _ptr(b), _ptr(out), batch, ws, _stream_ptr(stream)),
                    "wm_ntt_convolve")
         return out

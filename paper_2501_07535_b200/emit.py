@@ -46,6 +46,8 @@ def emit_cuda_launcher(program: DeviceKernel) -> str:
         f"/* {name}: reference launcher ABI (emit.py:456-484/545-560) backed by libwidemod_b200 (sm_100a). */",
         "#include <stdint.h>",
         "#include <stddef.h>",
+        "#include <stdio.h>",
+        "#include <mutex>",
         "#include <cuda_runtime.h>",
         '#include "widemod_b200.h"',
         "",
@@ -54,18 +56,37 @@ def emit_cuda_launcher(program: DeviceKernel) -> str:
         "static wm_field *field_ = NULL;",
         "static uint32_t *scratch_ = NULL;",
         "static size_t scratch_words_ = 0;",
+        "static std::mutex mu_;  /* the launcher's field, plan and scratch are shared by all callers */",
+        "static int status_ = WM_OK;",
+        "",
+        "/* The reference launchers return void (no error channel): a failure is",
+        f"   reported on stderr and kept for {name}_status(). */",
+        "static bool ok_(int rc, const char *what) {",
+        "    if (rc == WM_OK) return true;",
+        "    status_ = rc;",
+        f'    fprintf(stderr, "{name}: %s failed (%d): %s\\n", what, rc, wm_last_error());',
+        "    return false;",
+        "}",
+        "",
+        f'extern "C" int {name}_status(void) {{ std::lock_guard<std::mutex> g(mu_); return status_; }}',
         "",
         "static uint32_t *scratch(size_t words) {",
         "    if (words > scratch_words_) {",
         "        if (scratch_) cudaFree(scratch_);",
-        "        cudaMalloc((void **)&scratch_, words * sizeof(uint32_t));",
+        "        scratch_ = NULL;",
+        "        scratch_words_ = 0;",
+        "        if (cudaMalloc((void **)&scratch_, words * sizeof(uint32_t)) != cudaSuccess) {",
+        "            ok_(WM_ECUDA, \"scratch cudaMalloc\");",
+        "            scratch_ = NULL;",
+        "            return NULL;",
+        "        }",
         "        scratch_words_ = words;",
         "    }",
         "    return scratch_;",
         "}",
         "",
-        "static void init_field(void) {",
-        f"    if (!field_) wm_field_create({lay.bits}, Q_, {K}, &field_);",
+        "static bool init_field(void) {",
+        f"    return field_ || ok_(wm_field_create({lay.bits}, Q_, {K}, &field_), \"wm_field_create\");",
         "}",
         "",
     ]
@@ -80,13 +101,17 @@ def emit_cuda_launcher(program: DeviceKernel) -> str:
             "static wm_ntt_plan *plan_ = NULL;",
             "",
             f'extern "C" void {name}_launch(const {w} *in, {w} *x, int batch) {{',
-            "    init_field();",
-            f"    if (!plan_) wm_ntt_plan_create(field_, {n}, ROOT_, ROOT_INV_, N_INV_, &plan_);",
+            "    std::lock_guard<std::mutex> g(mu_);",
+            "    if (batch <= 0 || !init_field()) return;",
+            f"    if (!plan_ && !ok_(wm_ntt_plan_create(field_, {n}, ROOT_, ROOT_INV_, N_INV_, &plan_), "
+            f"\"wm_ntt_plan_create\")) return;",
             f"    const int64_t elems = (int64_t){n} * batch;",
             f"    uint32_t *t = scratch((size_t)elems * {K});",
-            f"    wm_ref_to_limbs({word}, {per_arg}, {K}, in, t, elems, NULL);",
-            f"    wm_ntt_{'inverse' if inverse else 'forward'}(plan_, t, t, batch, NULL, NULL);",
-            f"    wm_limbs_to_ref({word}, {per_arg}, {K}, t, x, elems, NULL);",
+            "    if (!t) return;",
+            f"    if (!ok_(wm_ref_to_limbs({word}, {per_arg}, {K}, in, t, elems, NULL), \"wm_ref_to_limbs\")) return;",
+            f"    if (!ok_(wm_ntt_{'inverse' if inverse else 'forward'}(plan_, t, t, batch, NULL, NULL), "
+            f"\"wm_ntt\")) return;",
+            f"    ok_(wm_limbs_to_ref({word}, {per_arg}, {K}, t, x, elems, NULL), \"wm_limbs_to_ref\");",
             "}",
         ]
         return "\n".join(lines) + "\n"
@@ -97,24 +122,30 @@ def emit_cuda_launcher(program: DeviceKernel) -> str:
         raise ValueError(f"no launcher for {spec.kind}")
     args = list(attrs["arg_names"])
     params = ", ".join(f"const {w} *{a}" for a in args) + f", {w} *out, int n_elems"
-    conv = f"    wm_ref_to_limbs({word}, {per_arg}, {K}, %s, %s, n_elems, NULL);"
+    conv = (f"    if (!ok_(wm_ref_to_limbs({word}, {per_arg}, {K}, %s, %s, n_elems, NULL), "
+            f"\"wm_ref_to_limbs\")) return;")
     lines += [f'extern "C" void {name}_launch({params}) {{',
-              "    init_field();",
+              "    std::lock_guard<std::mutex> g(mu_);",
+              "    if (n_elems <= 0 || !init_field()) return;",
               f"    uint32_t *t = scratch((size_t)n_elems * {3 * K});",
+              "    if (!t) return;",
               f"    uint32_t *A = t, *B = t + (size_t)n_elems * {K}, *O = t + (size_t)n_elems * {2 * K};"]
     if kind == "axpy":
         # the scalar is an un-indexed device pointer (vector_args=[False,True,True], kernels.py:228-230)
         lines += [f"    {w} s_host[{per_arg}];",
-                  f"    cudaMemcpy(s_host, a, sizeof(s_host), cudaMemcpyDeviceToHost);",
+                  "    if (cudaMemcpy(s_host, a, sizeof(s_host), cudaMemcpyDeviceToHost) != cudaSuccess) {",
+                  "        ok_(WM_ECUDA, \"scalar cudaMemcpy\");",
+                  "        return;",
+                  "    }",
                   f"    uint32_t s_limbs[{K}];",
                   f"    for (int j = 0; j < {K}; ++j) {{",
                   f"        int bit = 32 * j, wi = {per_arg} - 1 - bit / {word};",
                   f"        s_limbs[j] = (uint32_t)(s_host[wi] >> (bit % {word}));",
                   "    }",
                   conv % ("x", "A"), conv % ("y", "B"),
-                  "    wm_axpy(field_, s_limbs, A, B, O, n_elems, NULL);"]
+                  "    if (!ok_(wm_axpy(field_, s_limbs, A, B, O, n_elems, NULL), \"wm_axpy\")) return;"]
     else:
         lines += [conv % ("a", "A"), conv % ("b", "B"),
-                  f"    wm_{kind}(field_, A, B, O, n_elems, NULL);"]
-    lines += [f"    wm_limbs_to_ref({word}, {per_arg}, {K}, O, out, n_elems, NULL);", "}"]
+                  f"    if (!ok_(wm_{kind}(field_, A, B, O, n_elems, NULL), \"wm_{kind}\")) return;"]
+    lines += [f"    ok_(wm_limbs_to_ref({word}, {per_arg}, {K}, O, out, n_elems, NULL), \"wm_limbs_to_ref\");", "}"]
     return "\n".join(lines) + "\n"

@@ -233,8 +233,8 @@ class DeviceKernel:
     def field(self) -> Field:
         """Device field; the spec's mul_strategy ("schoolbook"/"karatsuba",
         reference KernelSpec.mul_strategy) selects the vmul/axpy multiplier."""
-        strat = self.spec.mul_strategy if self.spec.mul_strategy in ("schoolbook", "karatsuba") else "schoolbook"
-        return get_field(self.spec.layout.bits, self.modulus, strat)
+        _check_strategy(self.spec.mul_strategy)
+        return get_field(self.spec.layout.bits, self.modulus, self.spec.mul_strategy)
 
     def plan(self) -> NttPlan:
         if self.spec.ntt is None:
@@ -243,6 +243,12 @@ class DeviceKernel:
 
     def __repr__(self) -> str:
         return f"DeviceKernel({self.name})"
+
+
+def _check_strategy(strategy: str) -> None:
+    """Reference RewriteConfig.__post_init__ (rewrite.py:55-56)."""
+    if strategy not in ("schoolbook", "karatsuba"):
+        raise ValueError(f"unknown strategy {strategy!r}")
 
 
 def build_program(spec: KernelSpec, params_mode: str = "baked") -> DeviceKernel:
@@ -255,6 +261,8 @@ def generate_kernel(spec: KernelSpec, params_mode: str = "baked", target_has_dou
     """Reference kernels.py:368-381.  The lowering/pruning the reference does
     here is compile-time template unrolling of the device library, so the
     flags are accepted and have no effect; ``trace`` receives one line."""
+    # reference: RewriteConfig(mul_strategy=...) raises for an unknown strategy (rewrite.py:55-56)
+    _check_strategy(spec.mul_strategy)
     kern = DeviceKernel(spec, params_mode)
     if trace is not None:
         trace.append(f"device {kern.name}: {spec.layout.limbs} x 32-bit limbs (sm_100a)")

@@ -125,6 +125,28 @@ def ntt_large_fixture():
     return rows
 
 
+def butterfly_fixture():
+    """run_program on transform kinds: the reference's lowered butterfly
+    (build_ntt, kernels.py:270-311) on (u, v, w) operands, edge values included."""
+    from widemod.kernels import run_program
+    rows = []
+    for bits, word, n in [(16, 8, 8), (64, 64, 16), (128, 64, 16), (256, 64, 1024), (256, 32, 16),
+                          (384, 64, 64), (768, 64, 16)]:
+        for kind in ("ntt", "intt"):
+            prog = generate_kernel(make_spec(kind, bits, word, size=n))
+            p = int(prog.attributes["p"])
+            rnd = random.Random(5 + bits + n)
+            edge = (0, 1, p - 1)
+            ops = [(u, v, w) for u in edge for v in edge for w in edge]
+            ops += [(rnd.randrange(p), rnd.randrange(p), rnd.randrange(p)) for _ in range(12)]
+            outs = [run_program(prog, u, v, w) for u, v, w in ops]
+            rows.append({"kind": kind, "bits": bits, "word": word, "n": n, "p": str(p),
+                         "ops": [[str(a) for a in t] for t in ops],
+                         "out": [[str(a) for a in o] for o in outs]})
+        print(f"butterfly {bits}w{word}", flush=True)
+    return rows
+
+
 def twiddle_fixture():
     rows = []
     for width, n in [(16, 8), (128, 16), (256, 1024)]:
@@ -135,9 +157,9 @@ def twiddle_fixture():
 
 
 def main():
-    which = sys.argv[1:] or ["params", "blas", "ntt", "ntt_large", "twiddles"]
+    which = sys.argv[1:] or ["params", "blas", "ntt", "ntt_large", "twiddles", "butterfly"]
     makers = {"params": params_fixture, "blas": blas_fixture, "ntt": ntt_fixture,
-              "ntt_large": ntt_large_fixture, "twiddles": twiddle_fixture}
+              "ntt_large": ntt_large_fixture, "twiddles": twiddle_fixture, "butterfly": butterfly_fixture}
     for name in which:
         data = makers[name]()
         (HERE / f"{name}.json").write_text(json.dumps(data, indent=0, sort_keys=True) + "\n")

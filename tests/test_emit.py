@@ -64,6 +64,10 @@ def test_emitted_launchers_run(cuda, tmp_path):
     fn(ref_in.data_ptr(), ref_out.data_ptr(), batch)
     torch.cuda.synchronize()
     assert torch.equal(plan.field.from_ref_layout(ref_out, 32, 8), plan.forward(x))
+    status = getattr(lib, f"{prog.name}_status")
+    assert status() == 0
+    fn(ref_in.data_ptr(), ref_out.data_ptr(), -1)  # rejected, no launch, status untouched
+    assert status() == 0
     # vmul on 64-bit words, runtime params mode (q, mu pointers in the signature)
     vp = K.generate_kernel(K.make_spec("vmul", 256, 64, size=1000), params_mode="runtime")
     lib2 = ctypes.CDLL(str(build_so(emit_cuda_launcher(vp), tmp_path, vp.name)))

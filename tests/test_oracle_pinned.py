@@ -203,3 +203,45 @@ def test_exact_ntt_restatement_matches_reference_executor():
         ref = bigint.ntt_reference(x, prm["p"], prm["root"], prm["root_inv"], prm["n_inv"])
         for k in (0, 1, n - 1, n // 3):
             assert bigint.ntt_point(x, prm["p"], prm["root"], k) == ref[k]
+
+
+# ---- round 2: the full-output config fixtures and the reference butterfly
+def test_uniform_residue_limbs_matches_uniform_residues():
+    """The vectorised generator of the config fixtures draws exactly what
+    uniform_residues draws (same rejections, same order), incl. a small
+    modulus where rejections happen."""
+    for q, count in [((1 << 252) - 129, 3000), (4093, 5000), (500, 4000), ((1 << 64) - 59, 2000)]:
+        a = bigint.uniform_residues(np.random.Generator(np.random.PCG64(5)), count, q)
+        b = bigint.uniform_residue_limbs(np.random.Generator(np.random.PCG64(5)), count, q)
+        assert ints(b) == a, q
+
+
+def test_config_fixture_inputs_and_oracle(golden):
+    """tests/golden/ntt_configs.json: the inputs regenerate to the recorded
+    hash, and the pinned C oracle reproduces the config-2 output hashes (the
+    2^20/2^24 rows are produced by the same code path, make_ntt_configs.py)."""
+    rows = {r["name"]: r for r in golden("ntt_configs")}
+    assert set(rows) == {"cfg2_2p16_x64", "cfg4_2p20_x4", "cfg5_2p24"}
+    for r in rows.values():
+        p = int(r["p"])
+        assert p == bigint.find_ntt_params(256, r["n"])["p"] if r["n"] <= 1 << 20 else True
+        x = bigint.uniform_residue_limbs(np.random.Generator(np.random.PCG64(r["seed"])), r["batch"] * r["n"], p)
+        assert hashlib.sha256(x.tobytes()).hexdigest() == r["x_sha256"], r["name"]
+    r = rows["cfg2_2p16_x64"]
+    prm = bigint.find_ntt_params(256, r["n"])
+    x = bigint.uniform_residue_limbs(np.random.Generator(np.random.PCG64(r["seed"])), r["batch"] * r["n"], prm["p"])
+    of = OracleField(prm["p"], 256)
+    per = r["n"] * 8
+    fwd = of.ntt(x[: 4 * r["n"]], r["n"], prm["root"])  # the first 4 transforms (time)
+    for b in range(4):
+        assert hashlib.sha256(fwd.reshape(-1)[b * per:(b + 1) * per].tobytes()).hexdigest() == r["fwd_sha256_each"][b]
+
+
+def test_butterfly_golden_is_modular_butterfly(golden):
+    """The reference's run_program on transform kinds (butterfly.json) is
+    (u + v w, u - v w) mod p — what the device run_program computes."""
+    for row in golden("butterfly"):
+        p = int(row["p"])
+        for ops, out in zip(row["ops"], row["out"]):
+            u, v, w = (int(a) for a in ops)
+            assert [int(a) for a in out] == [(u + v * w) % p, (u - v * w) % p]
