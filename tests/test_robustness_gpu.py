@@ -141,6 +141,11 @@ def test_plan_creation_leaves_other_streams_running(cuda):
         torch.cuda._sleep(int(2e9))  # ~1 s of GPU clock cycles
         big.add_(1)
     prm = find_ntt_params(128, 1 << 10)
-    dev.NttPlan(dev.Field(128, prm.p), prm)
-    assert not side.query(), "plan creation waited for an unrelated stream"
+    # keep the plan alive past the check: destroying it frees device memory
+    # (cudaFree synchronises the device by definition)
+    plan = dev.NttPlan(dev.Field(128, prm.p), prm)
+    busy = not side.query()
+    torch.cuda.synchronize()
+    del plan
+    assert busy, "plan creation waited for an unrelated stream"
     side.synchronize()
