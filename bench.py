@@ -46,7 +46,14 @@ def log(*a):
 
 
 # ------------------------------------------------------------ distributed
-def dist_setup(gpus: int):
+DIST = {"backend": None}  # "nccl" | "gloo" once a process group exists
+
+
+def dist_setup(gpus: int, backend: str = "auto"):
+    """One process per GPU (torchrun).  backend "gloo" is the dry run of the
+    N>1 accounting where NCCL cannot run: ranks share the visible GPUs
+    (device = local rank mod device count), collectives go through host
+    memory.  Its timings are contended and only check the plumbing."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -58,15 +65,23 @@ def dist_setup(gpus: int):
         import torch
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        if _cuda_ok():
+        use_nccl = _cuda_ok() and backend in ("auto", "nccl")
+        if use_nccl:
             # bind the rank to its GPU before NCCL initialises (barriers and
             # collectives then use the right device)
             torch.cuda.set_device(local)
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            DIST["backend"] = "nccl"
         else:
             dist.init_process_group("gloo")
+            DIST["backend"] = "gloo"
         pg = dist
     return rank, world, local, pg
+
+
+def device_index(local: int) -> int:
+    import torch
+    return local % max(1, torch.cuda.device_count())
 
 
 def _cuda_ok():
@@ -83,7 +98,8 @@ def max_over_ranks(pg, value: float) -> float:
     if pg is None:
         return value
     import torch
-    t = torch.tensor([value], dtype=torch.float64, device="cuda" if _cuda_ok() else "cpu")
+    dev = "cuda" if (_cuda_ok() and DIST["backend"] == "nccl") else "cpu"
+    t = torch.tensor([value], dtype=torch.float64, device=dev)
     pg.all_reduce(t, op=pg.ReduceOp.MAX)
     return float(t.item())
 
@@ -185,7 +201,7 @@ def run_gpu(args, rank, world, local, pg):
     from paper_2501_07535_b200 import kernels as K
     from paper_2501_07535_b200.params import find_ntt_params
 
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(device_index(local))
     prm = find_ntt_params(BITS, N)
     plan = K.get_plan(BITS, prm)
     field = plan.field
@@ -222,7 +238,7 @@ def run_gpu(args, rank, world, local, pg):
     fwd_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     barrier(pg)
     torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
+    with ClockSampler(device_index(local)) as clocks:
         for s in range(args.steps):
             flush_l2(torch, flush)
             ev[s][0].record(stream)
@@ -250,7 +266,7 @@ def run_gpu(args, rank, world, local, pg):
     e2e = run_e2e(args, torch, plan, bufs, pg, world)
 
     # ---- extras: BLAS sweep (configs[2]), four-step single 2^24 NTT (configs[4]), reference GPU code
-    blas = run_blas(args, torch, field, pg) if not args.skip_extras else None
+    blas = run_blas(args, torch, field, rank, world, pg) if not args.skip_extras else None
     four = run_four_step(args, torch, rank, world, pg) if not args.skip_extras else None
     b20 = run_batched_2p20(args, torch, rank, world, pg) if not args.skip_extras else None
     refgpu = run_reference_gpu(args, torch, plan) if (world == 1 and not args.skip_extras) else None
@@ -351,57 +367,70 @@ def run_e2e(args, torch, plan, bufs, pg, world):
             "chunk_transforms": args.e2e_chunk or "auto"}
 
 
-def run_blas(args, torch, _field, pg):
+def run_blas(args, torch, _field, rank, world, pg):
     """BASELINE configs[2]: vadd/vmul/axpy n=2^24 at 128/256/384/768 bits,
     device-resident (inputs > L2), GB/s of algorithmic traffic (3 x 4K bytes
-    per element) vs the measured HBM copy bandwidth."""
+    per element) vs the measured HBM copy bandwidth.  The vector is sharded
+    by rank (contiguous n/P slices, no collective): every
+    rank runs its slice, the launch time is the max over ranks, GB/s is the
+    whole vector's bytes over that time.  vmul/axpy run with the reduction the
+    field selects (two-fold for these special-form moduli) and, beside it,
+    the generic Barrett path (reduction="barrett")."""
     from paper_2501_07535_b200 import device as dev
+    from paper_2501_07535_b200 import dist as D
     from paper_2501_07535_b200.params import find_ntt_params
     n = 1 << 24
+    lo, hi = D.shard_range(n, rank, world)
+    m = hi - lo
     hbm = peaks().get("hbm_gbs", 6650.0)
-    int_peak, _ = int_peak_wmul_per_s(None)
     out_rows = []
     stream = torch.cuda.current_stream()
     for bits in args.blas_bits:
         K = (bits + 31) // 32
         q = find_ntt_params(bits, 1).p
-        f = dev.Field(bits, q)
-        g = torch.Generator(device="cuda").manual_seed(bits)
-        a = torch.randint(-(1 << 31), 1 << 31, (n, K), dtype=torch.int32, device="cuda", generator=g)
-        b = torch.randint(-(1 << 31), 1 << 31, (n, K), dtype=torch.int32, device="cuda", generator=g)
+        g = torch.Generator(device="cuda").manual_seed(bits * 1000 + rank)
+        a = torch.randint(-(1 << 31), 1 << 31, (m, K), dtype=torch.int32, device="cuda", generator=g)
+        b = torch.randint(-(1 << 31), 1 << 31, (m, K), dtype=torch.int32, device="cuda", generator=g)
         top = (1 << (bits - 5 - 32 * (K - 1))) - 1
         a[:, K - 1] &= top
         b[:, K - 1] &= top
         out = torch.empty_like(a)
-        # multiplier strategy per width: Karatsuba wins from 8 limbs up (profiles/r01_ab_blas_mid_occupancy.txt)
-        fk = dev.Field(bits, q, "karatsuba") if K >= 8 else f
+        # multiplier strategy per width: Karatsuba from 8 limbs up (profiles/r02_ab_*.txt)
+        strat = "karatsuba" if K >= 8 else "schoolbook"
+        fields = {"vadd": [dev.Field(bits, q)],
+                  "vmul": [dev.Field(bits, q, strat), dev.Field(bits, q, strat, reduction="barrett")],
+                  "axpy": [dev.Field(bits, q, strat), dev.Field(bits, q, strat, reduction="barrett")]}
         for op in ("vadd", "vmul", "axpy"):
-            fm = fk if op in ("vmul", "axpy") else f
-            fn = (lambda: fm.axpy(123456789, a, b, out=out)) if op == "axpy" else \
-                (lambda op=op, fm=fm: getattr(fm, op)(a, b, out=out))
-            for _ in range(3):
-                fn()
-            torch.cuda.synchronize()
-            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(10)]
-            for e0, e1 in evs:
-                e0.record(stream)
-                fn()
-                e1.record(stream)
-            torch.cuda.synchronize()
-            ms = statistics.median(x.elapsed_time(y) for x, y in evs)
-            gbs = 3 * 4 * K * n / (ms * 1e-3) / 1e9
-            # binding roofline (SURVEY.md §8(d)): max(HBM time, integer time of the
-            # reference's 3k^2 word products per element) over the measured time
-            t_hbm = 3 * 4 * K * n / (hbm * 1e9)
-            t_int = (3 * K * K * n / int_peak) if op in ("vmul", "axpy") else 0.0
-            bound = "int" if t_int > t_hbm else "hbm"
-            out_rows.append({"op": op, "bits": bits, "n": n, "ms": round(ms, 4), "GB_per_s": round(gbs, 1),
-                             "hbm_frac_of_measured": round(gbs / hbm, 3), "strategy": fm.strategy,
-                             "binding": bound, "binding_frac": round(max(t_hbm, t_int) / (ms * 1e-3), 3)})
+            for fm in fields[op]:
+                fn = (lambda fm=fm: fm.axpy(123456789, a, b, out=out)) if op == "axpy" else \
+                    (lambda op=op, fm=fm: getattr(fm, op)(a, b, out=out))
+                for _ in range(3):
+                    fn()
+                torch.cuda.synchronize()
+                evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                       for _ in range(10)]
+                barrier(pg)
+                torch.cuda.synchronize()
+                for e0, e1 in evs:
+                    e0.record(stream)
+                    fn()
+                    e1.record(stream)
+                torch.cuda.synchronize()
+                ms = max_over_ranks(pg, statistics.median(x.elapsed_time(y) for x, y in evs))
+                gbs = 3 * 4 * K * n / (ms * 1e-3) / 1e9
+                row = {"op": op, "bits": bits, "n": n, "ms": round(ms, 4), "GB_per_s": round(gbs, 1),
+                       "hbm_frac_of_measured": round(gbs / (world * hbm), 3), "strategy": fm.strategy,
+                       "reduction": fm.reduction if op != "vadd" else None}
+                out_rows.append(row)
+        # parity of the benchmarked slice (both reductions, all ops) against each other
+        # is in tests/test_reduction_gpu.py; here a cheap cross-check of the last one
+        fa, fb = fields["vmul"]
+        assert torch.equal(fa.vmul(a[:4096], b[:4096]), fb.vmul(a[:4096], b[:4096])), "reduction mismatch"
         del a, b, out
-    return {"rows": out_rows, "hbm_measured_gbs": hbm, "int_peak_twmul_s": round(int_peak / 1e12, 3),
+    return {"rows": out_rows, "hbm_measured_gbs": hbm, "ranks": world,
+            "sharding": f"contiguous n/{world} slice per rank, no collective; ms = max over ranks",
             "note": "median of 10 launches; operands 0.8-4.8 GB (> L2); bytes = 2 reads + 1 write per element; "
-                    "binding_frac = max(bytes/HBM, 3k^2 products/int peak) / measured time"}
+                    "hbm_frac_of_measured = GB/s / (ranks x measured HBM copy bandwidth)"}
 
 
 def run_four_step(args, torch, rank, world, pg):
@@ -411,7 +440,12 @@ def run_four_step(args, torch, rank, world, pg):
     from paper_2501_07535_b200.params import find_ntt_params
     n = 1 << 24
     prm = find_ntt_params(BITS, n)
-    comm = D.TorchComm() if pg is not None else _SelfComm()
+    if pg is None:
+        comm = _SelfComm()
+    elif DIST["backend"] == "gloo":
+        comm = D.StagedComm()
+    else:
+        comm = D.TorchComm()
     eng = D.FourStepNtt(BITS, prm, rank, world, comm=comm)
     L = eng.layout
     rows = L.n1 // world
@@ -436,9 +470,14 @@ def run_four_step(args, torch, rank, world, pg):
     a2a_bytes = (world - 1) * (n // world) * 4 * K_LIMBS // world
     res = {"n": n, "ranks": world, "ms_per_forward": round(ms, 4), "us_per_transform": round(ms * 1e3, 2),
            "split": [L.n1, L.n2], "a2a_bytes_sent_per_rank": a2a_bytes,
-           "exchange": "NCCL all_to_all_single" if pg is not None else "local copy (one rank)",
+           "exchange": ("local copy (one rank)" if pg is None else
+                        "NCCL all_to_all_single" if DIST["backend"] == "nccl" else
+                        "host-staged gloo all_to_all_single (dry run: ranks share one GPU)"),
            "note": "max over ranks; forward only; input rows j1 per rank (scatter not timed)"}
-    res["fused"] = run_four_step_fused(torch, prm, rank, world, pg, x, y, reps)
+    if DIST["backend"] == "gloo":
+        res["fused"] = {"skipped": "symmetric-memory exchange needs one GPU per rank (gloo dry run)"}
+    else:
+        res["fused"] = run_four_step_fused(torch, prm, rank, world, pg, x, y, reps)
     del eng, x, y, back
     if world == 1:
         # the same transform through the single-GPU multi-pass plan (natural order in/out)
@@ -848,6 +887,8 @@ def main():
     ap.add_argument("--skip-extras", action="store_true", help="only the headline workload")
     ap.add_argument("--blas-bits", type=int, nargs="*", default=[128, 256, 384, 768])
     ap.add_argument("--e2e-chunk", type=int, default=0, help="transforms per host-pipeline chunk (0 = auto)")
+    ap.add_argument("--dist-backend", default="auto", choices=["auto", "nccl", "gloo"],
+                    help="N>1 process group: nccl (one GPU per rank) or gloo (dry run, ranks may share a GPU)")
     args = ap.parse_args()
     # stdout carries exactly one JSON line: anything libraries print there
     # (NCCL prints its version banner to stdout) goes to stderr instead
@@ -859,7 +900,7 @@ def main():
         log("note: warmup < 3 raised to 3")
         args.warmup = 3
 
-    rank, world, local, pg = dist_setup(args.gpus)
+    rank, world, local, pg = dist_setup(args.gpus, args.dist_backend)
     if args.impl == "reference":
         out = reference_arm(args, rank, world, pg)
         if rank == 0:
@@ -906,9 +947,9 @@ def main():
         "ns_per_butterfly_paper_metric": 2 * (res["ms_per_step"] * 1e6 / (2 * BATCH)) / (N * LOGN),
         "pipe_utilisation": pipes,
     }
-    cpu = None
-    if world == 1:
-        cpu = cpu_baseline_subprocess(args)
+    # the CPU baseline once, on rank 0, after every rank's GPU work (the other
+    # ranks wait at the final barrier)
+    cpu = cpu_baseline_subprocess(args)
     out = {
         "metric": METRIC,
         "value": res["us_per_transform"],

@@ -93,7 +93,22 @@ int wm_field_create(int bits, const uint32_t *q_host, int q_limbs, wm_field **ou
  * A width whose limb count has no Barrett kernels either (513-736, 769-992
  * bits) is created as such a padded Montgomery field when q is odd. */
 #define WM_FIELD_MONTGOMERY 2
+/* WM_FIELD_BARRETT: always reduce products by the generic Barrett quotient
+ * estimate (the reference's lower_modmul_barrett, rewrite.py:333-351).
+ * Without it, a reference-range modulus of special form q = 2^m - c with
+ * c < 2^32 (every modulus find_ntt_params returns, oracle.py:186-239: the
+ * largest primes below 2^(bits-4)) at 72 <= m and 4 <= 32K - m <= 31 is
+ * reduced by two folds t = H 2^m + L -> L + H c (K + 2 word products per
+ * product instead of ~1.5 K^2), in vmul/axpy and in the NTT butterflies.
+ * Results are the same canonical residues either way. */
+#define WM_FIELD_BARRETT 4
 int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags, wm_field **out);
+/* The reduction a field's products use: one of WM_REDUCTION_* (or a negative
+ * status on error). */
+#define WM_REDUCTION_BARRETT 0
+#define WM_REDUCTION_MONTGOMERY 1
+#define WM_REDUCTION_SPECIAL_FORM 2
+int wm_field_reduction(const wm_field *f);
 int wm_field_destroy(wm_field *f);
 int wm_field_info(const wm_field *f, int *bits, int *limbs, int *norm_shift);
 
@@ -216,6 +231,21 @@ int wm_scale_transpose_scatter(const wm_field *f, const uint32_t *in, const uint
                                void *stream);
 int wm_twiddle_table_2d(const wm_field *f, int64_t n, const uint32_t *root_host, int64_t row0,
                         int64_t rows, int64_t cols, uint32_t *table, void *stream);
+
+/* ---------------------------------------------------------------- diagnostics
+ * Roofline inputs for the integer-bound kernels (bench.py).
+ *   wm_probe_imad_wide: launch a kernel of 8 independent 32x32->64 product
+ *     chains per thread at full occupancy (mode 0: mad.wide.u32 with a 64-bit
+ *     addend, mode 1: mul.wide.u32), `iters` steps each; *products = word
+ *     products it executes.  Time it with events on `stream` for this GPU's
+ *     product throughput.  sink: 8 bytes of device scratch.
+ *   wm_ntt_pass_work: field multiplications the pass kernel `pass_index` of a
+ *     forward (inverse != 0: inverse) transform executes for `batch`
+ *     transforms, and the word products they cost in the plan's arithmetic
+ *     (32x32->32 low products count one half). */
+int wm_probe_imad_wide(int mode, int64_t iters, uint64_t *sink, void *stream, int64_t *products);
+int wm_ntt_pass_work(const wm_ntt_plan *p, int inverse, int pass_index, int64_t batch, int64_t *field_muls,
+                     double *word_products);
 
 /* ---------------------------------------------------------------- layout
  * Reference layout: AoS, `ref_words` words of `word_bits` (32 or 64) per

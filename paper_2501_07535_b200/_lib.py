@@ -19,7 +19,10 @@ WM_ECUDA = 2
 WM_EUNSUPPORTED = 3
 WM_ELENGTH = 4
 WM_NTT_FWD, WM_NTT_INV, WM_NTT_FWD_INV, WM_NTT_COPY = 0, 1, 2, 3
-WM_FIELD_KARATSUBA, WM_FIELD_MONTGOMERY = 1, 2
+WM_FIELD_KARATSUBA, WM_FIELD_MONTGOMERY, WM_FIELD_BARRETT = 1, 2, 4
+WM_REDUCTION_BARRETT, WM_REDUCTION_MONTGOMERY, WM_REDUCTION_SPECIAL_FORM = 0, 1, 2
+REDUCTION_NAMES = {WM_REDUCTION_BARRETT: "barrett", WM_REDUCTION_MONTGOMERY: "montgomery",
+                   WM_REDUCTION_SPECIAL_FORM: "special_form"}
 
 
 class LibraryUnavailable(RuntimeError):
@@ -52,6 +55,7 @@ SIGNATURES = [
     ("wm_field_create_ex", _int, [_int, _u32p, _int, _int, ctypes.POINTER(_vp)]),
     ("wm_field_destroy", _int, [_vp]),
     ("wm_field_info", _int, [_vp, ctypes.POINTER(_int), ctypes.POINTER(_int), ctypes.POINTER(_int)]),
+    ("wm_field_reduction", _int, [_vp]),
     ("wm_vadd", _int, [_vp, _vp, _vp, _vp, _i64, _vp]),
     ("wm_vsub", _int, [_vp, _vp, _vp, _vp, _i64, _vp]),
     ("wm_vmul", _int, [_vp, _vp, _vp, _vp, _i64, _vp]),
@@ -71,6 +75,8 @@ SIGNATURES = [
     ("wm_widemul", _int, [_int, _int, _vp, _vp, _vp, _i64, _vp]),
     ("wm_scale_transpose_scatter", _int, [_vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _i64, _i64, _vp]),
     ("wm_twiddle_table_2d", _int, [_vp, _i64, _u32p, _i64, _i64, _i64, _vp, _vp]),
+    ("wm_probe_imad_wide", _int, [_int, _i64, _vp, _vp, ctypes.POINTER(_i64)]),
+    ("wm_ntt_pass_work", _int, [_vp, _int, _int, _i64, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double)]),
     ("wm_ref_to_limbs", _int, [_int, _int, _int, _vp, _vp, _i64, _vp]),
     ("wm_limbs_to_ref", _int, [_int, _int, _int, _vp, _vp, _i64, _vp]),
 ]
@@ -97,6 +103,8 @@ def load(path: str | Path | None = None, build_if_missing: bool = True):
         except OSError as exc:
             raise LibraryUnavailable(f"cannot load {p}: {exc}") from exc
         for name, res, args in SIGNATURES:
+            if env and path is None and not hasattr(lib, name):
+                continue  # A/B variant built before a diagnostic export existed
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

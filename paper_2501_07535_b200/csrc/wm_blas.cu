@@ -160,6 +160,10 @@ struct BlasArgs {
 // STRAT: kSchoolbook / kKaratsuba Barrett products, or kMontField for fields
 // with a full-width modulus (Montgomery products, carry-aware add).
 constexpr int kMontField = 2;
+// Special-form fields (wm_field.pm): two-fold reduction after a schoolbook /
+// Karatsuba full product.
+constexpr int kPmField = 3;
+constexpr int kPmKara = 4;
 
 #ifndef WM_BLAS_MINB_WIDE  // resident CTAs requested for K >= 16 (register cap)
 #define WM_BLAS_MINB_WIDE 1
@@ -185,6 +189,19 @@ WM_DEV void blas_elem(uint32_t (&r)[K], const uint32_t (&x)[K], const uint32_t (
       uint32_t t[K];
       mont_mul<K>(t, args.scal, x, args.F.q, args.F.qinv);
       add_mod_full<K>(r, t, y, args.F.q);
+    }
+  } else if constexpr (STRAT == kPmField || STRAT == kPmKara) {
+    constexpr int PS = STRAT == kPmKara ? kKaratsuba : kSchoolbook;
+    if constexpr (OP == OP_VADD) {
+      add_mod<K>(r, x, y, args.F.q);
+    } else if constexpr (OP == OP_VSUB) {
+      sub_mod<K>(r, x, y, args.F.q);
+    } else if constexpr (OP == OP_VMUL) {
+      mul_pm<K, PS>(r, x, y, args.F);
+    } else {
+      uint32_t t[K];
+      mul_pm<K, PS>(t, args.scal, x, args.F);
+      add_mod<K>(r, t, y, args.F.q);
     }
   } else if constexpr (OP == OP_VADD) {
     add_mod<K>(r, x, y, args.F.q);
@@ -256,7 +273,7 @@ static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, 
   for (int j = 0; j < K; ++j) args.scal[j] = 0;
   if (scal_host) {
     const Big a(scal_host, scal_host + K);
-    const Big sh = f->mont ? to_mont(a, f->q) : big_shl(a, f->s, K);
+    const Big sh = f->mont ? to_mont(a, f->q) : (STRAT == kPmField || STRAT == kPmKara) ? a : big_shl(a, f->s, K);
     for (int j = 0; j < K; ++j) args.scal[j] = sh[j];
   }
   int64_t want = (n + 255) / 256;
@@ -293,6 +310,25 @@ static int blas_dispatch(int op, const wm_field *f, const uint32_t *a, const uin
       default:
         return fail(WM_EUNSUPPORTED, "limb count not built into the full-width (Montgomery) kernels");
     }
+  }
+  if (f->pm && (op == OP_VMUL || op == OP_AXPY)) {
+    switch (f->K) {
+#define WM_CASE(k)                                                                                 \
+  case k:                                                                                          \
+    if constexpr (k >= 3) {                                                                        \
+      if (op == OP_VMUL)                                                                           \
+        return f->karatsuba ? launch_blas<k, OP_VMUL, kPmKara>(f, a, b, out, n, nullptr, st)       \
+                            : launch_blas<k, OP_VMUL, kPmField>(f, a, b, out, n, nullptr, st);     \
+      return f->karatsuba ? launch_blas<k, OP_AXPY, kPmKara>(f, a, b, out, n, scal_host, st)       \
+                          : launch_blas<k, OP_AXPY, kPmField>(f, a, b, out, n, scal_host, st);     \
+    }                                                                                              \
+    break;
+      WM_BLAS_KS(WM_CASE)
+#undef WM_CASE
+      default:
+        break;
+    }
+    return fail(WM_EUNSUPPORTED, "limb count not built into the special-form kernels");
   }
   switch (f->K) {
 #define WM_CASE(k)                                                                                 \
@@ -443,7 +479,10 @@ int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags,
   int qb = big_bitlen(q);
   const int M = 32 * K - 4;
   if (qb < 2) return fail(WM_EINVAL, "modulus must exceed 1");
-  if (flags & ~(WM_FIELD_KARATSUBA | WM_FIELD_MONTGOMERY)) return fail(WM_EINVAL, "unknown field flags");
+  if (flags & ~(WM_FIELD_KARATSUBA | WM_FIELD_MONTGOMERY | WM_FIELD_BARRETT))
+    return fail(WM_EINVAL, "unknown field flags");
+  if ((flags & WM_FIELD_MONTGOMERY) && (flags & WM_FIELD_BARRETT))
+    return fail(WM_EINVAL, "WM_FIELD_BARRETT applies to reference-range fields only");
   if (flags & WM_FIELD_MONTGOMERY) {
     if (flags & WM_FIELD_KARATSUBA) return fail(WM_EINVAL, "Karatsuba applies to Barrett fields only");
     if (!mont_supports(K)) {  // zero-pad to the next limb count with Montgomery kernels
@@ -515,8 +554,28 @@ int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags,
   big_sub_inplace(f->nqn, f->qn);  // 2^(32K) - qn (mod 2^(32K))
   Big mu = big_pow2_div(2 * M, f->qn, K);
   f->mu8 = big_shl(mu, 3, K);
+  // special form q = 2^m - c, c < 2^32: two-fold reduction (mul_pm_lazy)
+  // unless the caller asked for the generic Barrett path
+  if (!(flags & WM_FIELD_BARRETT) && qb >= 72 && 32 * K - qb >= 4 && 32 * K - qb <= 31) {
+    Big two_m(K, 0u);
+    two_m[qb / 32] = 1u << (qb % 32);  // qb <= 32K - 4: bit qb lies inside K limbs
+    big_sub_inplace(two_m, q);         // 2^m - q (q < 2^m)
+    bool one_limb = true;
+    for (int j = 1; j < K; ++j) one_limb = one_limb && two_m[j] == 0u;
+    if (one_limb && two_m[0] != 0u) {
+      f->pm = true;
+      f->pm_c = two_m[0];
+      f->pm_sh = 32 * K - qb;
+    }
+  }
   *out = f;
   return WM_OK;
+}
+
+int wm_field_reduction(const wm_field *f) {
+  if (!f) return -fail(WM_EINVAL, "null field");
+  if (f->mont) return WM_REDUCTION_MONTGOMERY;
+  return f->pm ? WM_REDUCTION_SPECIAL_FORM : WM_REDUCTION_BARRETT;
 }
 
 int wm_field_destroy(wm_field *f) {

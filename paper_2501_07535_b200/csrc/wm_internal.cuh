@@ -86,6 +86,12 @@ struct wm_field {
   int K = 0;
   int s = 0;
   wm::Big q, qn, qn2, nqn, mu8;  // K limbs each
+  // special form q = 2^m - pm_c (pm_c < 2^32, 72 <= m, 4 <= 32K - m <= 31):
+  // vmul/axpy/NTT products reduce by two folds (mul_pm_lazy) unless the field
+  // was created with WM_FIELD_BARRETT; the Barrett constants stay valid
+  bool pm = false;
+  uint32_t pm_c = 0;
+  int pm_sh = 0;
 };
 
 struct wm_pass_plan {
@@ -119,7 +125,8 @@ struct wm_ntt_plan {
   uint32_t *tw_img = nullptr;
   std::vector<size_t> tw_img_off;
   size_t tw_img_words_dir = 0;
-  int mode = 0;        // Arith mode: 0 lazy Shoup [0,6p), 1 Montgomery, 2 Shoup [0,4p) (full-width p < 2^(32K-2))
+  int mode = 0;        // Arith mode: 0 lazy Shoup [0,6p), 1 Montgomery, 2 Shoup [0,4p) (full-width p < 2^(32K-2)),
+                       // 3 lazy special-form products [0,6p) (wm_field.pm)
   wm::Big ninv_mont;  // full-width fields: n^-1 R mod p (one-pass inverse scale)
   wm::Big ninv, ninv_sh, np, p2, p3, p4;  // n^-1, floor(n^-1 * 2^32K / p), 2^32K - p, 2p, 3p, 4p
   // internal workspace (used when the caller passes none): uses are
@@ -157,6 +164,8 @@ inline FieldConst<K> field_const(const wm_field *f) {
   }
   c.s = (uint32_t)f->s;
   c.qinv = f->qinv;
+  c.pm_c = f->pm_c;
+  c.pm_sh = (uint32_t)f->pm_sh;
   return c;
 }
 

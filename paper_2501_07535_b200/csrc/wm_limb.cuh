@@ -523,6 +523,8 @@ struct FieldConst {
   uint32_t nqn[K];  // 2^(32K) - qn
   uint32_t mu8[K];  // 8 * floor(2^(2M) / qn)
   uint32_t s;       // normalisation shift, 0..31
+  uint32_t pm_c;    // special-form fields: q = 2^m - pm_c
+  uint32_t pm_sh;   // special-form fields: 32K - m (4..31)
 };
 
 template <int K>
@@ -583,6 +585,69 @@ WM_DEV void mul_barrett(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t
   uint32_t as[K];
   shl_small<K>(as, a, F.s);
   mul_barrett_pre<K, barrett_style<K>(), STRAT>(r, as, b, F);
+}
+
+// ------------------------------------------------------------------ special-form moduli
+// q = 2^m - c with 1 <= c < 2^32, m = 32K - sh, 4 <= sh <= 31, m >= 72.  Every
+// modulus the reference's find_ntt_params returns has this form: the largest
+// prime (= 1 mod n) below 2^(bits-4), e.g. c = 59 / 129 / 65 / 393 for the
+// 128/256/384/768-bit BLAS moduli and c = k n - 1 < 2^32 for its NTT primes
+// (SURVEY.md §8 preamble).  With t = a b = H 2^m + L, t == L + H c (mod q);
+// two such folds (Crandall / Solinas reduction) cost K + 2 word products
+// instead of the ~1.5 K^2 of the Barrett quotient estimate:
+//   a < 2^(m+3) (lazy NTT values below 8q), b < 2^m:
+//   t < 2^(2m+3), H < 2^(m+3), s1 = L + H c < 2^(m+36) (K+1 limbs as sh >= 4)
+//   H2 = s1 >> m < 2^36, r = L2 + H2 c < 2^m + 2^68 < 2q (m >= 70)
+// For canonical a, b: H2 < 2^33 and r < 2^m + 2^65, so r - q < q and one
+// conditional subtraction makes r canonical.
+template <int K>
+WM_DEV void pm_reduce_wide(uint32_t (&r)[K], const uint32_t (&t)[2 * K], uint32_t c, uint32_t sh) {
+  const uint32_t rs = 32u - sh;             // m mod 32 (m div 32 = K - 1)
+  const uint32_t mask = 0xffffffffu >> sh;  // bits of limb K-1 below 2^m
+  uint32_t s[K + 1];
+  uint32_t carry = 0;
+#pragma unroll
+  for (int j = 0; j < K; ++j) {  // s = L + H c, H_j = bits [m + 32j, m + 32j + 32) of t
+    const uint32_t h = __funnelshift_r(t[K - 1 + j], t[K + j], rs);
+    const uint32_t l = (j == K - 1) ? (t[K - 1] & mask) : t[j];
+    const uint64_t p = (uint64_t)h * c + l + carry;
+    s[j] = (uint32_t)p;
+    carry = (uint32_t)(p >> 32);
+  }
+  s[K] = carry;
+  const uint32_t h0 = __funnelshift_r(s[K - 1], s[K], rs);  // H2 = s >> m = h0 + h1 2^32
+  const uint32_t h1 = s[K] >> rs;                           // < 2^4
+  const uint64_t p0 = (uint64_t)h0 * c;
+  const uint64_t p12 = (p0 >> 32) + (uint64_t)h1 * c;       // < 2^32 + 2^36
+  uint32_t y[K];
+  y[0] = (uint32_t)p0;
+  y[1] = (uint32_t)p12;
+  y[2] = (uint32_t)(p12 >> 32);
+#pragma unroll
+  for (int j = 3; j < K; ++j) y[j] = 0u;
+  uint32_t l2[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) l2[j] = (j == K - 1) ? (s[K - 1] & mask) : s[j];
+  add_n<K>(r, l2, y);
+}
+
+// Special-form product, lazy: r = a b mod q + {0, q}, r < 2q (bounds above).
+#ifndef WM_PM_STYLE
+#define WM_PM_STYLE kU64
+#endif
+template <int K, int STRAT = kSchoolbook, int ST = WM_PM_STYLE>
+WM_DEV void mul_pm_lazy(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K], uint32_t c,
+                        uint32_t sh) {
+  uint32_t t[2 * K];
+  mul_full_s<K, ST, STRAT>(t, a, b);
+  pm_reduce_wide<K>(r, t, c, sh);
+}
+
+// Canonical special-form product of canonical a, b.
+template <int K, int STRAT = kSchoolbook>
+WM_DEV void mul_pm(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K], const FieldConst<K> &F) {
+  mul_pm_lazy<K, STRAT>(r, a, b, F.pm_c, F.pm_sh);
+  cond_sub<K>(r, F.q);
 }
 
 // ------------------------------------------------------------------ full-width moduli

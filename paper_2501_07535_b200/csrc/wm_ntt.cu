@@ -161,7 +161,11 @@ int wm_ntt_plan_create(const wm_field *f, int64_t n, const uint32_t *root_host, 
   if (f->mont) pl->ninv_mont = to_mont(pl->ninv, f->q);
   // arithmetic mode: full-width fields with two bits of headroom take the
   // Shoup / [0, 4p) path, the rest the Montgomery path (Arith<K, MODE>)
-  pl->mode = !f->mont ? 0 : (big_bitlen(f->q) <= 32 * K - 2 ? 2 : 1);
+  // (special-form reference-range fields: MODE 3, two-fold products)
+#ifndef WM_PM_NTT
+#define WM_PM_NTT 1
+#endif
+  pl->mode = !f->mont ? ((WM_PM_NTT && f->pm && K >= 3) ? 3 : 0) : (big_bitlen(f->q) <= 32 * K - 2 ? 2 : 1);
   // Shoup companion of n^-1 and np = 2^(32K) - p on the host.
   {
     Big num = big_shl(pl->ninv, 32 * K, 2 * K);

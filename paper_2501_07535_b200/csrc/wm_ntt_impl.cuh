@@ -200,6 +200,39 @@ struct Arith<K, 2> {
   }
 };
 
+// MODE 3: reference-range fields of special form p = 2^m - c (wm_field.pm):
+// each twiddle product is a full product folded twice (mul_pm_lazy, K + 2
+// extra word products; result in [0, 2p)), the same lazy [0, 6p) window as
+// MODE 0 and no Shoup companions.
+#ifndef WM_PM_NTT_STRAT  // full product of the butterfly multiply
+#define WM_PM_NTT_STRAT kSchoolbook
+#endif
+template <int K>
+struct Arith<K, 3> {
+  static constexpr bool kWp = false;
+  WM_DEV static void bf(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&)[K],
+                        const NttConst<K> &c) {
+    uint32_t t[K];
+    mul_pm_lazy<K, WM_PM_NTT_STRAT>(t, x1, w, c.F.pm_c, c.F.pm_sh);
+    bf_finish<K>(x0, x1, t, c.p3);
+  }
+  WM_DEV static void bf1(uint32_t (&x0)[K], uint32_t (&x1)[K], const NttConst<K> &c) { bf_lazy_w1<K>(x0, x1, c.p3); }
+  WM_DEV static void twmul(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
+                           const uint32_t (&)[K], const NttConst<K> &c) {
+    mul_pm_lazy<K, WM_PM_NTT_STRAT>(r, v, w, c.F.pm_c, c.F.pm_sh);
+  }
+  WM_DEV static void canon(uint32_t (&v)[K], const NttConst<K> &c) { canonical_6p<K>(v, c.p, c.p2, c.p4); }
+  WM_DEV static void mulby(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&m)[K], const NttConst<K> &c) {
+    mul_pm<K>(r, v, m, c.F);
+  }
+};
+
+// Limb counts with a special-form NTT instantiation (m >= 72 needs K >= 3).
+template <int K>
+__host__ __device__ constexpr bool pm_ntt_built() {
+  return K >= 3;
+}
+
 // Limb counts with a full-width (Montgomery) NTT instantiation.
 template <int K>
 __host__ __device__ constexpr bool mont_ntt_built() {
@@ -814,6 +847,9 @@ int run_passes(const wm_ntt_plan *pl, bool inverse, const uint32_t *in, uint32_t
   if constexpr (mont_ntt_built<K>()) {
     if (pl->mode == 1) return run_passes_t<K, 1>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);
     if (pl->mode == 2) return run_passes_t<K, 2>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);
+  }
+  if constexpr (pm_ntt_built<K>()) {
+    if (pl->mode == 3) return run_passes_t<K, 3>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);
   }
   if (pl->mode != 0) return fail(WM_EUNSUPPORTED, "limb count not built into the full-width NTT kernels");
   return run_passes_t<K, 0>(pl, inverse, in, out, batch, ws, st, only_pass, mul_by);

@@ -85,12 +85,19 @@ class Field:
     (C ABI ``wm_field_*``).  Replaces the baked q/mu of a generated reference
     kernel (kernels._param_vars, kernels.py:168-181)."""
 
-    def __init__(self, bits: int, q: int, strategy: str = "schoolbook"):
+    def __init__(self, bits: int, q: int, strategy: str = "schoolbook", reduction: str = "auto"):
+        """strategy: full-product algorithm ("schoolbook"/"karatsuba") or a
+        full-width modulus ("montgomery").  reduction: "auto" reduces products
+        modulo a special-form q = 2^m - c (c < 2^32; every find_ntt_params
+        modulus) by two folds and any other q by Barrett; "barrett" forces the
+        generic Barrett path (WM_FIELD_BARRETT).  Results are identical."""
         self.lib = _lib.load()
         self.bits = int(bits)
         self.q = int(q)
         if strategy not in ("schoolbook", "karatsuba", "montgomery"):
             raise ValueError(f"unknown multiplication strategy {strategy!r}")
+        if reduction not in ("auto", "barrett"):
+            raise ValueError(f"unknown reduction {reduction!r}")
         self.strategy = strategy
         self.limbs = limbs_for_bits(self.bits)
         if self.q <= 1:
@@ -102,12 +109,19 @@ class Field:
         # products (the paper's full-width mode)
         flags = {"schoolbook": 0, "karatsuba": _lib.WM_FIELD_KARATSUBA,
                  "montgomery": _lib.WM_FIELD_MONTGOMERY}[strategy]
+        if reduction == "barrett":
+            flags |= _lib.WM_FIELD_BARRETT
         _lib.check(self.lib.wm_field_create_ex(self.bits, arr, self.limbs, flags, ctypes.byref(h)),
                    "wm_field_create_ex")
         self._h = h
         b, k, s = _i(), _i(), _i()
         _lib.check(self.lib.wm_field_info(self._h, ctypes.byref(b), ctypes.byref(k), ctypes.byref(s)))
         self.norm_shift = s.value
+        red = self.lib.wm_field_reduction(self._h)
+        if red < 0:
+            _lib.check(-red, "wm_field_reduction")
+        # the reduction the products use: "barrett", "montgomery" or "special_form"
+        self.reduction = _lib.REDUCTION_NAMES[red]
         # storage limbs: ceil(bits/32), or the zero-padded limb count of a
         # width without kernels of its own (run as a Montgomery field)
         self.limbs = k.value
@@ -195,6 +209,28 @@ class Field:
         _lib.check(self.lib.wm_limbs_to_ref(word_bits, ref_words, self.limbs, _ptr(limbs_t), _ptr(out), n,
                                             _stream_ptr(stream)))
         return out
+
+
+def probe_imad_wide(mode: int = 0, iters: int = 4096, stream=None) -> tuple[float, int]:
+    """Measured 32x32->64 word-product throughput of this GPU (products/s)
+    from wm_probe_imad_wide, timed with CUDA events; returns (rate, products)."""
+    torch = _torch()
+    lib = _lib.load()
+    sink = torch.zeros(1, dtype=torch.int64, device="cuda")
+    s = stream if stream is not None else torch.cuda.current_stream()
+    prods = ctypes.c_int64()
+    for _ in range(2):  # warm-up
+        _lib.check(lib.wm_probe_imad_wide(mode, iters, sink.data_ptr(), int(s.cuda_stream), ctypes.byref(prods)))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = None
+    for _ in range(5):
+        e0.record(s)
+        _lib.check(lib.wm_probe_imad_wide(mode, iters, sink.data_ptr(), int(s.cuda_stream), ctypes.byref(prods)))
+        e1.record(s)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1)
+        best = ms if best is None else min(best, ms)
+    return prods.value / (best * 1e-3), prods.value
 
 
 class NttPlan:
@@ -302,6 +338,16 @@ class NttPlan:
         _lib.check(self.lib.wm_ntt_pass(self._h, 1 if inverse else 0, pass_index, _ptr(x), _ptr(out), batch,
                                         _stream_ptr(stream)), "wm_ntt_pass")
         return out
+
+    def pass_work(self, pass_index: int, batch: int, inverse: bool = False) -> tuple[int, float]:
+        """(field multiplications, word products) one pass kernel executes
+        for `batch` transforms (wm_ntt_pass_work): the executed-work basis of
+        the NTT roofline."""
+        muls = ctypes.c_int64()
+        wp = ctypes.c_double()
+        _lib.check(self.lib.wm_ntt_pass_work(self._h, 1 if inverse else 0, pass_index, batch, ctypes.byref(muls),
+                                             ctypes.byref(wp)), "wm_ntt_pass_work")
+        return muls.value, wp.value
 
     def host_transform(self, host_in, host_out, mode: str = "forward", word_bits: int = 64,
                        ref_words: int | None = None, chunk: int = 0, stream=None):

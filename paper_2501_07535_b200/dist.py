@@ -121,6 +121,31 @@ class TorchComm:
         return out
 
 
+class StagedComm:
+    """all-to-all staged through host memory over a CPU process group (gloo):
+    the functional stand-in for TorchComm where NCCL cannot run, i.e. several
+    ranks sharing one GPU (2-process tests, ``bench.py --dist-backend gloo``
+    dry runs).  Same block layout as TorchComm; not a performance path."""
+
+    fused = False
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+
+    def all_to_all(self, out, inp):
+        import torch
+        torch.cuda.current_stream().synchronize()
+        src = inp.reshape(-1).cpu()
+        dst = torch.empty_like(src)
+        self.dist.all_to_all_single(dst, src, group=self.group)
+        out.view(-1).copy_(dst)
+        return out
+
+
 class SymmComm:
     """Peer-memory exchange for the four-step (the all-to-all fused into the
     twiddle/transpose kernel).  Every rank's receive buffer is allocated from
