@@ -187,11 +187,39 @@ def _alg_wmul(n: int) -> float:
     return (n // 2) * (n.bit_length() - 1) * ALG_WMUL_PER_BFLY
 
 
-def int_peak_wmul_per_s(sm_mhz: float | None):
-    """Integer-pipe roofline: 32 IMAD.WIDE (32x32->64 word products) per clock
-    per SM (measured half-rate, profiles/r01_imad_rate.jsonl) x 148 SMs."""
-    clk = 1965.0
-    return 32 * 148 * clk * 1e6, clk
+INT_PEAK = {}  # filled by measure_int_peak() on each rank
+
+
+def measure_int_peak():
+    """The integer roofline, measured in this run: 32x32->64 word products
+    per second of wm_probe_imad_wide (8 independent chains per thread, full
+    occupancy), best of the accumulate (mode 0) and plain (mode 1) forms."""
+    from paper_2501_07535_b200 import device as dev
+    r0, _ = dev.probe_imad_wide(0)
+    r1, _ = dev.probe_imad_wide(1)
+    INT_PEAK.update({"mad_wide_per_s": r0, "mul_wide_per_s": r1, "peak_per_s": max(r0, r1)})
+    return INT_PEAK["peak_per_s"]
+
+
+def int_peak_wmul_per_s(sm_mhz: float | None = None):
+    """Measured word-product peak (products/s); the nominal 32/clk/SM x 148
+    SMs x 1965 MHz only if the probe has not run."""
+    if "peak_per_s" in INT_PEAK:
+        return INT_PEAK["peak_per_s"], None
+    return 32 * 148 * 1965.0 * 1e6, 1965.0
+
+
+def plan_work(plan, batch: int, inverse: bool) -> float:
+    """Word products all passes of one direction execute for `batch`
+    transforms (wm_ntt_pass_work: executed work in the plan's arithmetic)."""
+    return sum(plan.pass_work(i, batch, inverse)[1] for i in range(len(plan.pass_log_sizes)))
+
+
+EXTRAS = ("generic", "blas", "four_step", "batched", "reference_gpu", "full_width", "steady")
+
+
+def want(args, name: str) -> bool:
+    return not args.skip_extras and name in args.extras
 
 
 def run_gpu(args, rank, world, local, pg):
@@ -216,6 +244,7 @@ def run_gpu(args, rank, world, local, pg):
                         chunk=args.e2e_chunk)
     torch.cuda.synchronize()
 
+    measure_int_peak()
     x = canonical_random(torch, BATCH * N, 1234 + rank)
     y = torch.empty_like(x)
     z = torch.empty_like(x)
@@ -262,25 +291,56 @@ def run_gpu(args, rank, world, local, pg):
 
     pass0_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
 
+    # ---- the same step through the generic Barrett/Shoup path (reduction="barrett")
+    generic = None
+    if want(args, "generic"):
+        from paper_2501_07535_b200 import device as dev
+        gplan = dev.NttPlan(dev.Field(BITS, prm.p, reduction="barrett"), prm)
+        gws = torch.empty(max(1, gplan.workspace_bytes(BATCH) // 4), dtype=torch.int32, device="cuda")
+        for _ in range(args.warmup):
+            gplan.forward(x, out=y, workspace=gws)
+            gplan.inverse(y, out=z, workspace=gws)
+        torch.cuda.synchronize()
+        assert torch.equal(z, x), "generic-path roundtrip mismatch"
+        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier(pg)
+        torch.cuda.synchronize()
+        for s in range(args.steps):
+            flush_l2(torch, flush)
+            gev[s][0].record(stream)
+            gplan.forward(x, out=y, workspace=gws)
+            gplan.inverse(y, out=z, workspace=gws)
+            gev[s][1].record(stream)
+        torch.cuda.synchronize()
+        gms = max_over_ranks(pg, sum(a.elapsed_time(b) for a, b in gev))
+        generic = {"us_per_transform": gms * 1e3 / transforms, "reduction": "barrett",
+                   "note": "the headline step with WM_FIELD_BARRETT: Shoup butterflies (MODE 0), same inputs, "
+                           "same timing protocol"}
+        del gplan, gws
+
     # ---- end-to-end through the C ABI with host buffers (reference layout)
     e2e = run_e2e(args, torch, plan, bufs, pg, world)
 
     # ---- extras: BLAS sweep (configs[2]), four-step single 2^24 NTT (configs[4]), reference GPU code
-    blas = run_blas(args, torch, field, rank, world, pg) if not args.skip_extras else None
-    four = run_four_step(args, torch, rank, world, pg) if not args.skip_extras else None
-    b20 = run_batched_2p20(args, torch, rank, world, pg) if not args.skip_extras else None
-    refgpu = run_reference_gpu(args, torch, plan) if (world == 1 and not args.skip_extras) else None
-    fullw = run_full_width(args, torch) if not args.skip_extras else None
-    steady = run_steady_state(args, torch, plan) if not args.skip_extras else None
+    blas = run_blas(args, torch, field, rank, world, pg) if want(args, "blas") else None
+    four = run_four_step(args, torch, rank, world, pg) if want(args, "four_step") else None
+    b20 = run_batched_2p20(args, torch, rank, world, pg) if want(args, "batched") else None
+    refgpu = run_reference_gpu(args, torch, plan) if (world == 1 and want(args, "reference_gpu")) else None
+    fullw = run_full_width(args, torch) if want(args, "full_width") else None
+    steady = run_steady_state(args, torch, plan) if want(args, "steady") else None
 
     return {
         "us_per_transform": us_per_transform,
         "ms_per_step": total_ms / args.steps,
         "pass0_ms": pass0_ms,
+        "pass0_work": plan.pass_work(0, BATCH, False),
+        "plan_mode": {"special_form": 3, "barrett": 0}.get(field.reduction, "?"),
+        "reduction": field.reduction,
         "pass_log_sizes": plan.pass_log_sizes,
         "launches_per_step": launches_per_step,
         "clocks": clocks.summary(),
         "e2e": e2e,
+        "generic": generic,
         "blas": blas,
         "four_step": four,
         "batched_2p20": b20,
@@ -495,8 +555,9 @@ def run_four_step(args, torch, rank, world, pg):
         e1.record(stream)
         torch.cuda.synchronize()
         res["single_gpu_plan_ms_per_forward"] = round(e0.elapsed_time(e1) / reps, 4)
-        res["single_gpu_plan_int_roofline_frac"] = round(
-            _alg_wmul(n) / (e0.elapsed_time(e1) / reps * 1e-3) / int_peak_wmul_per_s(None)[0], 3)
+        t = e0.elapsed_time(e1) / reps * 1e-3
+        res["single_gpu_plan_int_frac_executed"] = round(plan_work(plan, 1, False) / t / int_peak_wmul_per_s()[0], 3)
+        res["single_gpu_plan_int_frac_reference_work"] = round(_alg_wmul(n) / t / int_peak_wmul_per_s()[0], 3)
         res["single_gpu_plan_passes"] = plan.pass_log_sizes
         del xs, ys, ws
     torch.cuda.empty_cache()
@@ -653,9 +714,12 @@ def run_batched_2p20(args, torch, rank, world, pg):
     torch.cuda.empty_cache()
     return {"n": n, "batch_total": total, "ranks": world, "ms_fwd_plus_inv": round(ms, 3),
             "us_per_transform": round(ms * 1e3 / (2 * total), 2), "passes": plan.pass_log_sizes,
-            "int_roofline_frac": round(_alg_wmul(n) * 2 * (total // world) / (ms * 1e-3) / int_peak_wmul_per_s(None)[0], 3),
-            "int_roofline_basis": "reference algorithmic work (3k^2 products per butterfly) / time / per-GPU integer "
-                                  "peak; above 1 because Shoup + lazy reduction execute ~0.5 of those products",
+            "int_frac_executed": round((plan_work(plan, b, False) + plan_work(plan, b, True)) / (ms * 1e-3)
+                                       / int_peak_wmul_per_s()[0], 3),
+            "int_frac_reference_work": round(_alg_wmul(n) * 2 * b / (ms * 1e-3) / int_peak_wmul_per_s()[0], 3),
+            "int_frac_basis": "word products / time / measured per-GPU product peak (max over ranks' time); "
+                              "executed = the plan's own products (wm_ntt_pass_work), reference_work = 3k^2 per "
+                              "butterfly (SURVEY.md \u00a78(d); above the executed work)",
             "scaling": "strong (fixed total batch 256)", "note": "max over ranks; inputs 8 GiB / world per rank"}
 
 
@@ -885,6 +949,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=2 * BATCH,
                     help="transforms per CPU-baseline step (default: the whole batch-64 fwd+inv step)")
     ap.add_argument("--skip-extras", action="store_true", help="only the headline workload")
+    ap.add_argument("--extras", nargs="*", default=list(EXTRAS), choices=list(EXTRAS),
+                    help="which extra measurements to run (default: all)")
     ap.add_argument("--blas-bits", type=int, nargs="*", default=[128, 256, 384, 768])
     ap.add_argument("--e2e-chunk", type=int, default=0, help="transforms per host-pipeline chunk (0 = auto)")
     ap.add_argument("--dist-backend", default="auto", choices=["auto", "nccl", "gloo"],
@@ -916,33 +982,43 @@ def main():
             pg.destroy_process_group()
         return
 
-    # roofline of the dominant kernel: ntt_col_pass (pass 0), integer pipe
+    # roofline of the dominant kernel: ntt_col_pass (pass 0), integer pipe.
+    # achieved = word products the launch executes (wm_ntt_pass_work) / its
+    # event-timed duration; peak = this run's measured product throughput.
     sizes = res["pass_log_sizes"]
-    peak, clk = int_peak_wmul_per_s(res["clocks"].get("sm_mhz"))
+    peak, _ = int_peak_wmul_per_s()
     pass_ms = res["pass0_ms"]
+    muls, wprod = res["pass0_work"]
+    achieved = wprod / (pass_ms * 1e-3)
     bflies = BATCH * (N // 2) * sizes[0]  # one pass = log2(L) radix-2 stages over the batch
-    achieved = bflies * ALG_WMUL_PER_BFLY / (pass_ms * 1e-3)
+    ref_achieved = bflies * ALG_WMUL_PER_BFLY / (pass_ms * 1e-3)
+    kname = f"ntt_col_pass<8, {res['plan_mode']}>"
     traffic = None
     pipes = None
     try:
-        prof = json.loads((ROOT / "profiles" / "r01_ncu_traffic.json").read_text())
-        kp = prof.get("ntt_col_pass<8, 0>") or prof["ntt_col_pass<8>"]
+        prof = json.loads((ROOT / "profiles" / "r02_ncu_traffic.json").read_text())
+        kp = prof[kname]
         traffic = kp["dram_bytes_per_launch"]
         pipes = {"fmaheavy_pct": kp.get("fmaheavy_pct"), "alu_pct": kp.get("alu_pct"),
-                 "basis": "ncu --set full of the same kernel (profiles/r01_ncu_traffic.json): the "
-                          "IMAD/IMAD.WIDE (FMA-heavy) pipe is the binding unit; the kernels execute ~0.5 "
-                          "of the reference's 3k^2 products per butterfly (Shoup + lazy reduction)"}
+                 "basis": "ncu --set full of the same kernel (profiles/r02_ncu_traffic.json)"}
     except Exception:
         pass
     roofline = {
-        "bound": "int", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Twmul/s",
+        "bound": "int", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "T word-products/s",
         "frac": achieved / peak, "traffic": traffic,
-        "kernel": f"ntt_col_pass<8, 0> (pass 0 of {'+'.join('2^%d' % s for s in sizes)}), batch 64, {pass_ms * 1e3:.1f} us/launch",
-        "work": f"{ALG_WMUL_PER_BFLY} word products per butterfly (reference 3k^2, SURVEY.md \u00a78(d)) x "
-                f"batch*(n/2)*log2(L) butterflies per launch = {bflies * ALG_WMUL_PER_BFLY:.4g}",
-        "peak_basis": f"32 IMAD.WIDE/clk/SM x 148 SMs x {clk:.0f} MHz (half-rate IMAD.WIDE measured, "
-                      f"profiles/r01_imad_rate.jsonl)",
-        "traffic_basis": "dram__bytes_read+write per launch, ncu --set full (profiles/r01_ncu_traffic.json); "
+        "kernel": f"{kname} (pass 0 of {'+'.join('2^%d' % s for s in sizes)}), batch 64, "
+                  f"{pass_ms * 1e3:.1f} us/launch",
+        "work": f"{muls} field multiplications x {wprod / max(1, muls):.0f} word products (32x32->64) each = "
+                f"{wprod:.4g} per launch, as executed (wm_ntt_pass_work; two-fold special-form products)",
+        "peak_basis": "32x32->64 products/s measured in this run by wm_probe_imad_wide (best of mad.wide/"
+                      f"mul.wide chains at full occupancy: {INT_PEAK.get('mul_wide_per_s', 0) / 1e12:.3f} / "
+                      f"{INT_PEAK.get('mad_wide_per_s', 0) / 1e12:.3f} T/s)",
+        "reference_work_basis": {"achieved": ref_achieved / 1e12, "frac": ref_achieved / peak,
+                                 "work": f"{ALG_WMUL_PER_BFLY} products per butterfly (reference 3k^2, SURVEY.md "
+                                         f"\u00a78(d)) x {bflies} butterflies",
+                                 "note": "the reference algorithm's products; the kernel executes fewer, so this "
+                                         "fraction can exceed 1"},
+        "traffic_basis": "dram__bytes_read+write per launch, ncu --set full (profiles/r02_ncu_traffic.json); "
                          "algorithmic bytes per launch = 2 x 128 MiB",
         "ns_per_butterfly_paper_metric": 2 * (res["ms_per_step"] * 1e6 / (2 * BATCH)) / (N * LOGN),
         "pipe_utilisation": pipes,
@@ -966,12 +1042,18 @@ def main():
         "config": {"workload": "256-bit forward+inverse NTT n=2^16 batch 64 per GPU (BASELINE configs[1])",
                    "bits": BITS, "n": N, "batch_per_gpu": BATCH, "transforms_per_step": 2 * BATCH,
                    "parallelism": f"batch-sharded x{world}", "l2": "flushed between timed steps (252 MiB write)",
+                   "reduction": f"{res['reduction']} (p = 2^252 - c, c < 2^32: two-fold products; "
+                                "headline_generic_barrett = the same step on the generic path)",
+                   "dist_backend": DIST["backend"],
                    "passes": sizes},
         "e2e": res["e2e"],
         "gpu_launches": res["launches_per_step"] * args.steps,
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": res["clocks"],
+        "int_peak_measured": {k: round(v / 1e12, 4) for k, v in INT_PEAK.items()},
+        "reduction": res["reduction"],
+        "headline_generic_barrett": res["generic"],
         "blas": res["blas"],
         "four_step_2p24": res["four_step"],
         "batched_2p20_x256": res["batched_2p20"],

@@ -216,10 +216,13 @@ int wm_ntt_plan_create(const wm_field *f, int64_t n, const uint32_t *root_host, 
 
 int wm_ntt_plan_destroy(wm_ntt_plan *p) {
   if (!p) return WM_OK;
-  if (p->tw_fwd) cudaFree(p->tw_fwd);
-  if (p->tw_inv) cudaFree(p->tw_inv);
-  if (p->tw_inv_scaled) cudaFree(p->tw_inv_scaled);
-  if (p->tw_img) cudaFree(p->tw_img);
+  // the tables come from the stream-ordered allocator (plan creation must not
+  // serialise other streams); destruction keeps cudaFree's semantics: wait
+  // for every user on the device, then return them to the pool
+  if (p->tw_fwd || p->tw_inv || p->tw_inv_scaled || p->tw_img) cudaDeviceSynchronize();
+  for (uint32_t *t : {p->tw_fwd, p->tw_inv, p->tw_inv_scaled, p->tw_img})
+    if (t) cudaFreeAsync(t, cudaStreamLegacy);
+  if (p->tw_fwd || p->tw_inv || p->tw_inv_scaled || p->tw_img) cudaStreamSynchronize(cudaStreamLegacy);
   if (p->ws) cudaFree(p->ws);
   if (p->ws_ev) cudaEventDestroy(p->ws_ev);
   release_host_pipeline(p);

@@ -204,22 +204,30 @@ struct Arith<K, 2> {
 // each twiddle product is a full product folded twice (mul_pm_lazy, K + 2
 // extra word products; result in [0, 2p)), the same lazy [0, 6p) window as
 // MODE 0 and no Shoup companions.
-#ifndef WM_PM_NTT_STRAT  // full product of the butterfly multiply
-#define WM_PM_NTT_STRAT kSchoolbook
+// Full product of the butterfly multiply: Karatsuba for 8..16 limbs
+// (profiles/r02_ab_pm.txt: 256-bit 2^16 8.66 -> 8.54 us/transform), schoolbook
+// elsewhere (WM_PM_NTT_STRAT forces one for A/B runs).
+template <int K>
+__host__ __device__ constexpr int pm_ntt_strat() {
+#ifdef WM_PM_NTT_STRAT
+  return WM_PM_NTT_STRAT;
+#else
+  return (K >= 8 && K <= 16) ? kKaratsuba : kSchoolbook;
 #endif
+}
 template <int K>
 struct Arith<K, 3> {
   static constexpr bool kWp = false;
   WM_DEV static void bf(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&)[K],
                         const NttConst<K> &c) {
     uint32_t t[K];
-    mul_pm_lazy<K, WM_PM_NTT_STRAT>(t, x1, w, c.F.pm_c, c.F.pm_sh);
+    mul_pm_lazy<K, pm_ntt_strat<K>()>(t, x1, w, c.F.pm_c, c.F.pm_sh);
     bf_finish<K>(x0, x1, t, c.p3);
   }
   WM_DEV static void bf1(uint32_t (&x0)[K], uint32_t (&x1)[K], const NttConst<K> &c) { bf_lazy_w1<K>(x0, x1, c.p3); }
   WM_DEV static void twmul(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
                            const uint32_t (&)[K], const NttConst<K> &c) {
-    mul_pm_lazy<K, WM_PM_NTT_STRAT>(r, v, w, c.F.pm_c, c.F.pm_sh);
+    mul_pm_lazy<K, pm_ntt_strat<K>()>(r, v, w, c.F.pm_c, c.F.pm_sh);
   }
   WM_DEV static void canon(uint32_t (&v)[K], const NttConst<K> &c) { canonical_6p<K>(v, c.p, c.p2, c.p4); }
   WM_DEV static void mulby(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&m)[K], const NttConst<K> &c) {
@@ -859,8 +867,10 @@ template <int K>
 static int create_tables_on(wm_ntt_plan *pl, const Big &root, const Big &root_inv, cudaStream_t st) {
   const int64_t n = pl->n;
   const size_t bytes = (size_t)n * 2 * K * sizeof(uint32_t);
-  WM_CUDA_TRY(cudaMalloc(&pl->tw_fwd, bytes));
-  WM_CUDA_TRY(cudaMalloc(&pl->tw_inv, bytes));
+  // stream-ordered allocations: cudaMalloc would serialise every stream of
+  // the device (implicit synchronisation on allocation)
+  WM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&pl->tw_fwd), bytes, st));
+  WM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&pl->tw_inv), bytes, st));
   Big one(K, 0u);
   one[0] = 1;
   int rc = gen_table<K>(pl->field, pl->tw_fwd, n, root, one, pl->mode, st);
@@ -868,7 +878,7 @@ static int create_tables_on(wm_ntt_plan *pl, const Big &root, const Big &root_in
   rc = gen_table<K>(pl->field, pl->tw_inv, n, root_inv, one, pl->mode, st);
   if (rc) return rc;
   if (pl->passes.size() > 1) {
-    WM_CUDA_TRY(cudaMalloc(&pl->tw_inv_scaled, bytes));
+    WM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&pl->tw_inv_scaled), bytes, st));
     rc = gen_table<K>(pl->field, pl->tw_inv_scaled, n, root_inv, pl->ninv, pl->mode, st);
     if (rc) return rc;
   }
@@ -880,7 +890,7 @@ static int create_tables_on(wm_ntt_plan *pl, const Big &root, const Big &root_in
     words += twimg_bytes(K, ps.logL) / sizeof(uint32_t);
   }
   pl->tw_img_words_dir = words;
-  WM_CUDA_TRY(cudaMalloc(&pl->tw_img, 2 * words * sizeof(uint32_t)));
+  WM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&pl->tw_img), 2 * words * sizeof(uint32_t), st));
   WM_CUDA_TRY(cudaMemsetAsync(pl->tw_img, 0, 2 * words * sizeof(uint32_t), st));
   for (int dir = 0; dir < 2; ++dir) {
     const uint32_t *table = dir ? pl->tw_inv : pl->tw_fwd;

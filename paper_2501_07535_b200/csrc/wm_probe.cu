@@ -72,8 +72,10 @@ extern "C" int wm_probe_imad_wide(int mode, int64_t iters, uint64_t *sink, void 
 static int64_t half_products_per_mul(const wm_ntt_plan *p) {
   const int64_t K = p->K;
   switch (p->mode) {
-    case 3:  // full product K^2 + fold 1 (K) + fold 2 (2)
-      return 2 * (K * K + K + 2);
+    case 3: {  // full product (schoolbook K^2 / one Karatsuba level 3 (K/2)^2) + folds (K + 2)
+      const int64_t full = (K >= 8 && K <= 16 && K % 2 == 0) ? 3 * (K / 2) * (K / 2) : K * K;
+      return 2 * (full + K + 2);
+    }
     case 0:
     case 2: {  // Shoup: truncated high half + two low halves (K(K-1)/2 wide + K lo each)
       const int64_t C0 = K > 2 ? K - 2 : 0;
