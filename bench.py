@@ -455,11 +455,13 @@ def run_blas(args, torch, _field, rank, world, pg):
         a[:, K - 1] &= top
         b[:, K - 1] &= top
         out = torch.empty_like(a)
-        # multiplier strategy per width: Karatsuba from 8 limbs up (profiles/r02_ab_*.txt)
-        strat = "karatsuba" if K >= 8 else "schoolbook"
+        # full-product strategy per width and reduction (profiles/r02_ab_pm.txt):
+        # special form: Karatsuba from 12 limbs; Barrett: from 8 limbs
+        sp = "karatsuba" if K >= 12 else "schoolbook"
+        sb = "karatsuba" if K >= 8 else "schoolbook"
         fields = {"vadd": [dev.Field(bits, q)],
-                  "vmul": [dev.Field(bits, q, strat), dev.Field(bits, q, strat, reduction="barrett")],
-                  "axpy": [dev.Field(bits, q, strat), dev.Field(bits, q, strat, reduction="barrett")]}
+                  "vmul": [dev.Field(bits, q, sp), dev.Field(bits, q, sb, reduction="barrett")],
+                  "axpy": [dev.Field(bits, q, sp), dev.Field(bits, q, sb, reduction="barrett")]}
         for op in ("vadd", "vmul", "axpy"):
             for fm in fields[op]:
                 fn = (lambda fm=fm: fm.axpy(123456789, a, b, out=out)) if op == "axpy" else \
@@ -756,47 +758,66 @@ def run_reference_gpu(args, torch, plan):
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / reps
 
-    # vmul 2^24, reference layout (8 x 32-bit words, MSW first) == 32 B/element
-    n = 1 << 24
-    q = find_ntt_params(BITS, 1).p
-    f = dev.Field(BITS, q)
-    a = canonical_random(torch, n, 11)
-    b = canonical_random(torch, n, 12)
-    ra, rb = f.to_ref_layout(a, 32, 8), f.to_ref_layout(b, 32, 8)
-    rout = torch.empty_like(ra)
+    # BLAS 2^24: vadd/vmul/axpy x 128/256/384/768 bits x runtime/baked q, mu
+    # in the reference layout (32-bit words MSW first, padded
+    # to a power of two), each output checked against ours
     from paper_2501_07535_b200.params import compute_barrett
-    mu = compute_barrett(q, BITS).mu
-    muw = torch.tensor([w - (1 << 32) if w >= 1 << 31 else w for w in K.to_words(mu, 8, 32)],
-                       dtype=torch.int32).cuda()
-    qw = torch.tensor([w - (1 << 32) if w >= 1 << 31 else w for w in K.to_words(q, 8, 32)],
-                      dtype=torch.int32).cuda()
-    lib.vmul16777216_256w32_runtime_launch.argtypes = [vp, vp, vp, vp, vp, i]
-    lib.refdrv_vmul16777216_256w32_runtime.argtypes = [vp, vp, vp, vp, vp, i, i]
-    lib.refdrv_vmul16777216_256w32_baked.argtypes = [vp, vp, vp, i, i]
-    # the reference's own launcher (1024 threads/block): does it launch at all?
-    rout.zero_()
-    torch.cuda.synchronize()
-    lib.vmul16777216_256w32_runtime_launch(ra.data_ptr(), rb.data_ptr(), qw.data_ptr(), muw.data_ptr(),
-                                           rout.data_ptr(), n)
-    torch.cuda.synchronize()
-    launch_err = "kernel did not run (output untouched)" if not bool(rout.any()) else "ran"
+    n = 1 << 24
     thr = 256
-    ms_rt = timed(lambda: lib.refdrv_vmul16777216_256w32_runtime(ra.data_ptr(), rb.data_ptr(), qw.data_ptr(),
-                                                                  muw.data_ptr(), rout.data_ptr(), n, thr))
-    ok_rt = torch.equal(f.from_ref_layout(rout, 32, 8), f.vmul(a, b))
-    ms_bk = timed(lambda: lib.refdrv_vmul16777216_256w32_baked(ra.data_ptr(), rb.data_ptr(), rout.data_ptr(), n,
-                                                               thr))
-    ok_bk = torch.equal(f.from_ref_layout(rout, 32, 8), f.vmul(a, b))
-    ours = dev.Field(BITS, q)
-    out = torch.empty_like(a)
-    ms_ours = timed(lambda: ours.vmul(a, b, out=out))
-    gb = 3 * 32 * n / 1e9
-    res["vmul_2p24"] = {"reference_runtime_q_GBps": round(gb / (ms_rt * 1e-3), 1),
-                        "reference_baked_q_GBps": round(gb / (ms_bk * 1e-3), 1),
-                        "ours_GBps": round(gb / (ms_ours * 1e-3), 1),
-                        "reference_matches_ours": bool(ok_rt and ok_bk),
-                        "reference_launcher_1024_threads_error": str(launch_err),
-                        "speedup_vs_reference_runtime": round(ms_rt / ms_ours, 2)}
+    rows = []
+    names = {"vadd": ["a", "b"], "vmul": ["a", "b"], "axpy": ["a", "x", "y"]}
+    extra = {"vadd": ["q"], "vmul": ["q", "mu"], "axpy": ["q", "mu"]}
+
+    def words_dev(v, P):
+        return torch.tensor([w - (1 << 32) if w >= 1 << 31 else w for w in K.to_words(v, P, 32)],
+                            dtype=torch.int32).cuda()
+
+    for bits in args.blas_bits:
+        Kl = bits // 32
+        P = 1 << (Kl - 1).bit_length()
+        q = find_ntt_params(bits, 1).p
+        mu = compute_barrett(q, bits).mu
+        f = dev.Field(bits, q, "karatsuba" if Kl >= 12 else "schoolbook")
+        g = torch.Generator(device="cuda").manual_seed(bits + 5)
+        a = torch.randint(-(1 << 31), 1 << 31, (n, Kl), dtype=torch.int32, device="cuda", generator=g)
+        b = torch.randint(-(1 << 31), 1 << 31, (n, Kl), dtype=torch.int32, device="cuda", generator=g)
+        a[:, Kl - 1] &= (1 << (bits - 5 - 32 * (Kl - 1))) - 1
+        b[:, Kl - 1] &= (1 << (bits - 5 - 32 * (Kl - 1))) - 1
+        ra, rb = f.to_ref_layout(a, 32, P), f.to_ref_layout(b, 32, P)
+        rout = torch.empty_like(ra)
+        scal = 123456789
+        dv = {"a": ra, "b": rb, "x": ra, "y": rb, "q": words_dev(q, P), "mu": words_dev(mu, P),
+              "s": words_dev(scal, P)}
+        out = torch.empty_like(a)
+        gb = 3 * 4 * Kl * n / 1e9
+        for kind in ("vadd", "vmul", "axpy"):
+            ours = (lambda: f.axpy(scal, a, b, out=out)) if kind == "axpy" else \
+                (lambda kind=kind: getattr(f, kind)(a, b, out=out))
+            ms_ours = timed(ours)
+            want = out.clone()
+            for mode in ("runtime", "baked"):
+                name = f"{kind}{n}_{bits}w32_{mode}"
+                fn = getattr(lib, "refdrv_" + name, None)
+                if fn is None:
+                    rows.append({"kind": kind, "bits": bits, "mode": mode, "unavailable": "not built"})
+                    continue
+                argn = names[kind] + (extra[kind] if mode == "runtime" else [])
+                fn.argtypes = [vp] * (len(argn) + 1) + [i, i]
+                # axpy's `a` is the scalar: one element in the reference layout
+                ptrs = [(dv["s"] if (kind == "axpy" and nm == "a") else dv[nm]).data_ptr() for nm in argn]
+                rout.zero_()
+                ms_ref = timed(lambda: fn(*ptrs, rout.data_ptr(), n, thr))
+                ok = bool(torch.equal(f.from_ref_layout(rout, 32, P), want))
+                rows.append({"kind": kind, "bits": bits, "mode": mode, "reference_GBps": round(gb / (ms_ref * 1e-3), 1),
+                             "ours_GBps": round(gb / (ms_ours * 1e-3), 1), "speedup": round(ms_ref / ms_ours, 2),
+                             "reference_matches_ours": ok})
+        del a, b, ra, rb, rout, out, dv
+    res["blas_2p24"] = {"rows": rows, "n": n, "ours": "auto reduction (special form), bench strategies",
+                        "bytes": "algorithmic 3 x bits/8 per element for both (the reference layout pads "
+                                 "384/768-bit values to 16/32 words)",
+                        "reference_driver": f"emitted {{kind}}_kernel at {thr} threads/block (its own launcher's "
+                                            "1024 threads/block does not launch from 256 bits)"}
+    torch.cuda.empty_cache()
     # NTT 2^11 (largest the reference's emitted CUDA compiles at 256 bits), batch 512
     nn, batch = 1 << 11, 512
     prm = find_ntt_params(BITS, nn)

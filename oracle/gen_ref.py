@@ -25,9 +25,10 @@ REF_SRC = Path("/root/reference/pkg/src")
 
 # reference GPU kernels (emit_cuda text compiled for sm_100a): (kind, bits, word, size, params_mode).
 # The NTT is the largest size whose __constant__ twiddle table still fits (2^11 at 256 bits).
-GPU_KERNELS = [("vmul", 256, 32, 1 << 24, "runtime"), ("vmul", 256, 32, 1 << 24, "baked"),
-               ("vadd", 256, 32, 1 << 24, "baked"), ("ntt", 256, 32, 1 << 11, "baked"),
-               ("intt", 256, 32, 1 << 11, "baked")]
+# BLAS: vadd/vmul/axpy x 128/256/384/768 bits x baked/runtime q, mu (kernels.py:168-181).
+GPU_KERNELS = ([(kind, bits, 32, 1 << 24, mode) for kind in ("vadd", "vmul", "axpy") for bits in (128, 256, 384, 768)
+                for mode in ("runtime", "baked")]
+               + [("ntt", 256, 32, 1 << 11, "baked"), ("intt", 256, 32, 1 << 11, "baked")])
 
 # (kind, bits, word, size): the bench workload's transforms and the BLAS sweep
 NTT_KERNELS = [("ntt", 256, 64, 1 << 16), ("intt", 256, 64, 1 << 16)]
@@ -130,8 +131,9 @@ def build_gpu(emit_cuda_fn=None) -> None:
     import shutil
     from widemod.emit import emit_cuda
     from widemod.kernels import generate_kernel, make_spec
+    from concurrent.futures import ThreadPoolExecutor
     nvcc = shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
-    objs = []
+    jobs = []
     for kind, bits, word, size, mode in GPU_KERNELS:
         prog = generate_kernel(make_spec(kind, bits, word, size=size), params_mode=mode)
         src = emit_cuda(prog)
@@ -146,11 +148,18 @@ def build_gpu(emit_cuda_fn=None) -> None:
         src += _gpu_driver(prog, name, kind, size)
         f = OUT / f"{name}.emitted.cu"
         f.write_text(src)
+        jobs.append((name, f))
+
+    def compile_one(job):
+        name, f = job
         o = f.with_suffix(".o")
         subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-Xcompiler", "-fPIC",
-                        "-c", str(f), "-o", str(o)], check=True)
-        objs.append(str(o))
+                        "-c", str(f), "-o", str(o)], check=True, capture_output=True)
         print(f"gen_ref: compiled reference CUDA {name}", flush=True)
+        return str(o)
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(compile_one, jobs))
     lib = OUT / "libref_gpu.so"
     subprocess.run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(lib), *objs],
                    check=True)

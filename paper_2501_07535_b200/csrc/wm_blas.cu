@@ -409,6 +409,52 @@ __global__ void limbs_to_ref_kernel(int word_bits, int R, int K, const uint32_t 
   }
 }
 
+template <int K>
+constexpr bool mont_blas_built() {
+#define WM_EQ(k) || K == k
+  return false WM_MONT_KS(WM_EQ);
+#undef WM_EQ
+}
+
+template <int K, int STRAT>
+static void preload_blas_k() {
+  cudaFuncAttributes a;
+  (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_VADD, STRAT == kMontField ? kMontField : kSchoolbook>);
+  (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_VSUB, STRAT == kMontField ? kMontField : kSchoolbook>);
+  (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_VMUL, STRAT>);
+  (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_AXPY, STRAT>);
+}
+
+void preload_field(const wm_field *f) {
+  switch (f->K) {
+#define WM_CASE(k)                                                                       \
+  case k:                                                                                \
+    if (f->mont) {                                                                       \
+      if constexpr (mont_blas_built<k>()) preload_blas_k<k, kMontField>();               \
+    } else if (f->pm) {                                                                  \
+      if constexpr (k >= 3) {                                                            \
+        if (f->karatsuba) preload_blas_k<k, kPmKara>(); else preload_blas_k<k, kPmField>(); \
+      }                                                                                  \
+    } else if (f->karatsuba) {                                                           \
+      preload_blas_k<k, kKaratsuba>();                                                   \
+    } else {                                                                             \
+      preload_blas_k<k, kSchoolbook>();                                                  \
+    }                                                                                    \
+    break;
+    WM_BLAS_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      break;
+  }
+  {
+    cudaFuncAttributes a;
+    (void)cudaFuncGetAttributes(&a, (const void *)ref_to_limbs_kernel);
+    (void)cudaFuncGetAttributes(&a, (const void *)limbs_to_ref_kernel);
+  }
+  preload_ntt(f);
+  (void)cudaGetLastError();  // best effort: creating a field needs no device
+}
+
 }  // namespace wm
 
 using namespace wm;
@@ -455,6 +501,7 @@ int wm_supported_limbs(int ntt, int *out, int cap) {
 int wm_field_create(int bits, const uint32_t *q_host, int q_limbs, wm_field **out) {
   return wm_field_create_ex(bits, q_host, q_limbs, 0, out);
 }
+
 
 int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags, wm_field **out) {
   if (!out) return fail(WM_EINVAL, "null output pointer");
@@ -529,6 +576,7 @@ int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags,
     Big one(K, 0u);
     one[0] = 1;
     f->r2 = big_shl_mod(one, 64 * K, q);
+    preload_field(f);
     *out = f;
     return WM_OK;
   }
@@ -568,6 +616,7 @@ int wm_field_create_ex(int bits, const uint32_t *q_host, int q_limbs, int flags,
       f->pm_sh = 32 * K - qb;
     }
   }
+  preload_field(f);
   *out = f;
   return WM_OK;
 }

@@ -169,6 +169,11 @@ inline FieldConst<K> field_const(const wm_field *f) {
   return c;
 }
 
+int ntt_mode_for(const wm_field *f);
+// Load the kernel images a field's BLAS calls and transforms use (CUDA lazy
+// loading synchronises the context on a kernel's first load); best effort.
+void preload_ntt(const wm_field *f);
+void preload_field(const wm_field *f);
 int ntt_run_internal(const wm_ntt_plan *p, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
                      void *workspace, cudaStream_t st, const uint32_t *mul_by = nullptr);
 int release_host_pipeline(wm_ntt_plan *p);

@@ -8,6 +8,33 @@ namespace wm {
 WM_NTT_KS(WM_EXTERN_INST)
 #undef WM_EXTERN_INST
 
+// Arithmetic mode of a field's transforms: full-width fields with two bits of
+// headroom take the Shoup / [0, 4p) path (2), the other full-width fields the
+// Montgomery path (1); special-form reference-range fields the two-fold
+// products (3), the rest Shoup / [0, 6p) (0).
+#ifndef WM_PM_NTT
+#define WM_PM_NTT 1
+#endif
+int ntt_mode_for(const wm_field *f) {
+  if (f->mont) return big_bitlen(f->q) <= 32 * f->K - 2 ? 2 : 1;
+  return (WM_PM_NTT && f->pm && f->K >= 3) ? 3 : 0;
+}
+
+void preload_ntt(const wm_field *f) {
+  if (!ntt_supports(f->K)) return;
+  const int mode = ntt_mode_for(f);
+  switch (f->K) {
+#define WM_CASE(k)            \
+  case k:                     \
+    ntt_preload<k>(mode);     \
+    break;
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      break;
+  }
+}
+
 static int plan_passes(wm_ntt_plan *pl) {
   const int K = pl->K;
   const int logn = pl->logn;
@@ -161,11 +188,7 @@ int wm_ntt_plan_create(const wm_field *f, int64_t n, const uint32_t *root_host, 
   if (f->mont) pl->ninv_mont = to_mont(pl->ninv, f->q);
   // arithmetic mode: full-width fields with two bits of headroom take the
   // Shoup / [0, 4p) path, the rest the Montgomery path (Arith<K, MODE>)
-  // (special-form reference-range fields: MODE 3, two-fold products)
-#ifndef WM_PM_NTT
-#define WM_PM_NTT 1
-#endif
-  pl->mode = !f->mont ? ((WM_PM_NTT && f->pm && K >= 3) ? 3 : 0) : (big_bitlen(f->q) <= 32 * K - 2 ? 2 : 1);
+  pl->mode = ntt_mode_for(f);
   // Shoup companion of n^-1 and np = 2^(32K) - p on the host.
   {
     Big num = big_shl(pl->ninv, 32 * K, 2 * K);

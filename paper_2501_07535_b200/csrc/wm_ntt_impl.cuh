@@ -939,7 +939,47 @@ int extract_twiddles(const wm_ntt_plan *p, int inverse, int64_t count, uint32_t 
 
 // Explicit instantiations live in wm_ntt_k*.cu (one limb-count group per
 // translation unit, compiled in parallel); wm_ntt.cu sees them as extern.
+// Load this limb count's NTT kernel images for arithmetic mode `mode`.  With
+// CUDA's lazy loading the first launch of a kernel loads its image, which
+// synchronises the context; wm_field_create_ex calls this (best effort) so
+// plan creation and the first transforms never wait for other streams.
+template <int K>
+int ntt_preload(int mode) {
+  cudaFuncAttributes a;
+  auto touch = [&](const void *fn) { (void)cudaFuncGetAttributes(&a, fn); };
+  touch((const void *)twiddle_image_kernel<K>);
+  if (mode == 1 || mode == 2) {
+    if constexpr (mont_ntt_built<K>()) {
+      touch((const void *)twiddle_gen_kernel<K, true>);
+      touch((const void *)twiddle_gen_kernel<K, true, true>);
+      touch((const void *)twiddle_extract_kernel<K, true>);
+      if (mode == 1) {
+        touch((const void *)ntt_col_pass<K, 1>);
+        touch((const void *)ntt_row_pass<K, 1>);
+      } else {
+        touch((const void *)ntt_col_pass<K, 2>);
+        touch((const void *)ntt_row_pass<K, 2>);
+      }
+    }
+  } else {
+    touch((const void *)twiddle_gen_kernel<K, false>);
+    touch((const void *)twiddle_extract_kernel<K, false>);
+    if (mode == 3) {
+      if constexpr (pm_ntt_built<K>()) {
+        touch((const void *)ntt_col_pass<K, 3>);
+        touch((const void *)ntt_row_pass<K, 3>);
+      }
+    } else {
+      touch((const void *)ntt_col_pass<K, 0>);
+      touch((const void *)ntt_row_pass<K, 0>);
+    }
+  }
+  (void)cudaGetLastError();  // best effort: no device is not an error here
+  return WM_OK;
+}
+
 #define WM_NTT_INSTANTIATE(PREFIX, k)                                                                      \
+  PREFIX template int ntt_preload<k>(int);                                                                 \
   PREFIX template int run_passes<k>(const wm_ntt_plan *, bool, const uint32_t *, uint32_t *, int64_t,      \
                                     uint32_t *, cudaStream_t, int, const uint32_t *);                      \
   PREFIX template int create_tables<k>(wm_ntt_plan *, const Big &, const Big &);                           \

@@ -134,16 +134,19 @@ def test_plan_creation_leaves_other_streams_running(cuda):
     torch = cuda
     from paper_2501_07535_b200 import device as dev
     from paper_2501_07535_b200.params import find_ntt_params
+    # the field loads its kernel images (CUDA lazy loading synchronises the
+    # context on a kernel's first load), so it is created before the side work
+    prm = find_ntt_params(128, 1 << 10)
+    field = dev.Field(128, prm.p)
     side = torch.cuda.Stream()
     big = torch.empty(1 << 28, dtype=torch.int32, device="cuda")
     torch.cuda.synchronize()
     with torch.cuda.stream(side):
         torch.cuda._sleep(int(2e9))  # ~1 s of GPU clock cycles
         big.add_(1)
-    prm = find_ntt_params(128, 1 << 10)
     # keep the plan alive past the check: destroying it frees device memory
     # (cudaFree synchronises the device by definition)
-    plan = dev.NttPlan(dev.Field(128, prm.p), prm)
+    plan = dev.NttPlan(field, prm)
     busy = not side.query()
     torch.cuda.synchronize()
     del plan

@@ -16,6 +16,8 @@ KEYS = [
     ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smem_wavefronts"),
     ("sm__inst_issued.avg.pct_of_peak_sustained_elapsed", "issue_pct"),
     ("smsp__inst_executed.sum", "warp_instructions"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "alu_inst_pct"),
+    ("sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active", "fma_inst_pct"),
     ("dram__bytes_read.sum", "dram_read_bytes"),
     ("dram__bytes_write.sum", "dram_write_bytes"),
     ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct"),
@@ -37,8 +39,10 @@ def summarise(rep):
     rows = list(csv.reader(io.StringIO(txt)))
     hdr = rows[0]
     units = dict(zip(hdr, rows[1]))
+    # bytes -> bytes; durations -> microseconds (ncu prints "us"/"ms"/"ns")
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
-             "nsecond": 1, "usecond": 1e3, "msecond": 1e6}
+             "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6,
+             "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6}
     out = []
     for row in rows[2:]:
         d = dict(zip(hdr, row))
@@ -47,7 +51,7 @@ def summarise(rep):
             if k in d:
                 try:
                     v = float(d[k].replace(",", ""))
-                    v *= scale.get(units.get(k, ""), 1)  # bytes -> bytes, time -> ns
+                    v *= scale.get(units.get(k, ""), 1)
                     rec[name] = v
                 except ValueError:
                     rec[name] = d[k]

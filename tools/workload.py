@@ -17,6 +17,8 @@ def main():
     ap.add_argument("--logn", type=int, default=None)
     ap.add_argument("--batch", type=int, default=64)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--strategy", default=None, help="schoolbook/karatsuba (default: the bench's choice)")
+    ap.add_argument("--reduction", default="auto", choices=["auto", "barrett"])
     a = ap.parse_args()
     import torch
     from paper_2501_07535_b200 import device as dev
@@ -32,7 +34,8 @@ def main():
 
     if a.what == "ntt":
         logn = a.logn or 16
-        plan = K.get_plan(a.bits, find_ntt_params(a.bits, 1 << logn))
+        prm = find_ntt_params(a.bits, 1 << logn)
+        plan = dev.NttPlan(dev.Field(a.bits, prm.p, reduction=a.reduction), prm)
         x = rand(a.batch << logn, 1)
         y = torch.empty_like(x)
         ws = torch.empty(max(1, plan.workspace_bytes(a.batch) // 4), dtype=torch.int32, device="cuda")
@@ -41,7 +44,9 @@ def main():
             plan.inverse(y, out=x, workspace=ws)
     else:
         logn = a.logn or 24
-        f = dev.Field(a.bits, find_ntt_params(a.bits, 1).p)
+        kara_from = 12 if a.reduction == "auto" else 8  # the bench's choice (bench.py run_blas)
+        strat = a.strategy or ("karatsuba" if Kl >= kara_from and a.what != "vadd" else "schoolbook")
+        f = dev.Field(a.bits, find_ntt_params(a.bits, 1).p, strat, reduction=a.reduction)
         x, y = rand(1 << logn, 1), rand(1 << logn, 2)
         out = torch.empty_like(x)
         for _ in range(a.reps):
