@@ -86,5 +86,30 @@ def build(force: bool = False, verbose: bool = False, variant: str | None = None
     return lib_path
 
 
+def build_conv(force: bool = False) -> Path:
+    """The CPython extension _wmconv (csrc/host/wm_conv.c): Python int <->
+    limb marshalling for the drop-in run_vector / run_ntt calls."""
+    import sysconfig
+    src = CSRC / "host" / "wm_conv.c"
+    out = PKG / ("_wmconv" + sysconfig.get_config_var("EXT_SUFFIX"))
+    stamp = PKG / ".wmconv.stamp"
+    digest = hashlib.sha256(src.read_bytes()).hexdigest()
+    if not force and out.exists() and stamp.exists() and stamp.read_text().strip() == digest:
+        return out
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if not cc:
+        raise RuntimeError("no C compiler for _wmconv")
+    inc = sysconfig.get_paths()["include"]
+    tmp = out.with_suffix(".tmp")
+    res = subprocess.run([cc, "-O2", "-shared", "-fPIC", f"-I{inc}", str(src), "-o", str(tmp)],
+                         capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"_wmconv build failed:\n{res.stderr}")
+    os.replace(tmp, out)
+    stamp.write_text(digest)
+    return out
+
+
 if __name__ == "__main__":
     print(build(verbose=True))
+    print(build_conv())

@@ -28,20 +28,33 @@ def limbs_for_bits(bits: int) -> int:
     return (bits + 31) // 32
 
 
+try:  # C loop over the interpreter's int <-> bytes conversions (csrc/host/wm_conv.c)
+    from . import _wmconv
+except ImportError:  # not built on this host: the same conversion per element in Python
+    _wmconv = None
+
+
 def ints_to_limbs(values: Iterable[int], limbs: int) -> np.ndarray:
-    """Python ints -> uint32 array [len, limbs], little-endian limbs."""
+    """Python ints -> uint32 array [len, limbs], little-endian limbs
+    (reference to_words, kernels.py:418-421, without the MSW-first order)."""
     nbytes = 4 * limbs
     try:
-        buf = b"".join(int(v).to_bytes(nbytes, "little") for v in values)
+        if _wmconv is not None:
+            vals = values if isinstance(values, (list, tuple)) else list(values)
+            buf = _wmconv.ints_to_limbs(vals, limbs)
+        else:
+            buf = b"".join(int(v).to_bytes(nbytes, "little") for v in values)
     except OverflowError as exc:
         raise ValueError(f"value does not fit in {limbs} limbs (or is negative)") from exc
     return np.frombuffer(buf, dtype="<u4").reshape(-1, limbs).copy()
 
 
 def limbs_to_ints(arr: np.ndarray) -> list[int]:
-    """uint32 array [len, limbs] -> Python ints."""
+    """uint32 array [len, limbs] -> Python ints (reference from_words)."""
     a = np.ascontiguousarray(arr, dtype="<u4")
     limbs = a.shape[-1]
+    if _wmconv is not None:
+        return _wmconv.limbs_to_ints(a.reshape(-1), limbs)
     raw = a.tobytes()
     step = 4 * limbs
     return [int.from_bytes(raw[i:i + step], "little") for i in range(0, len(raw), step)]
