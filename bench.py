@@ -215,7 +215,7 @@ def plan_work(plan, batch: int, inverse: bool) -> float:
     return sum(plan.pass_work(i, batch, inverse)[1] for i in range(len(plan.pass_log_sizes)))
 
 
-EXTRAS = ("generic", "blas", "four_step", "batched", "reference_gpu", "full_width", "steady")
+EXTRAS = ("generic", "blas", "four_step", "batched", "reference_gpu", "full_width", "steady", "drop_in")
 
 
 def want(args, name: str) -> bool:
@@ -328,6 +328,7 @@ def run_gpu(args, rank, world, local, pg):
     refgpu = run_reference_gpu(args, torch, plan) if (world == 1 and want(args, "reference_gpu")) else None
     fullw = run_full_width(args, torch) if want(args, "full_width") else None
     steady = run_steady_state(args, torch, plan) if want(args, "steady") else None
+    dropin = run_drop_in(args, torch) if (rank == 0 and want(args, "drop_in")) else None
 
     return {
         "us_per_transform": us_per_transform,
@@ -347,6 +348,7 @@ def run_gpu(args, rank, world, local, pg):
         "reference_gpu": refgpu,
         "full_width": fullw,
         "steady_state": steady,
+        "drop_in": dropin,
     }
 
 
@@ -493,6 +495,101 @@ def run_blas(args, torch, _field, rank, world, pg):
             "sharding": f"contiguous n/{world} slice per rank, no collective; ms = max over ranks",
             "note": "median of 10 launches; operands 0.8-4.8 GB (> L2); bytes = 2 reads + 1 write per element; "
                     "hbm_frac_of_measured = GB/s / (ranks x measured HBM copy bandwidth)"}
+
+
+def run_drop_in(args, torch):
+    """The reference-facing calls: run_vector and
+    run_ntt on Python ints at n = 2^16, 256 bits (BASELINE configs[0], one
+    transform of configs[1]) — int -> limb conversion, H2D, kernels, D2H,
+    limb -> int — and wm_blas_host on pinned host buffers in the reference
+    layout at n = 2^24 (end-to-end BLAS GB/s beside its PCIe floor)."""
+    from paper_2501_07535_b200 import device as dev
+    from paper_2501_07535_b200 import kernels as K
+    from paper_2501_07535_b200.params import find_ntt_params
+    res = {}
+    q = find_ntt_params(BITS, 1).p
+    rng = np.random.Generator(np.random.PCG64(21))
+    limbs = rng.integers(0, 1 << 32, size=(2 * N, K_LIMBS), dtype=np.uint64).astype(np.uint32)
+    limbs[:, -1] &= (1 << 27) - 1
+    vals = dev.limbs_to_ints(limbs)
+    xs, ys = vals[:N], vals[N:]
+    prog = K.generate_kernel(K.make_spec("vmul", BITS, 64, size=N))
+
+    def wall(fn, reps):
+        fn()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            out = fn()
+            ts.append(time.perf_counter() - t0)
+        return statistics.median(ts), out
+
+    t, out = wall(lambda: K.run_vector(prog, xs, ys), 5)
+    assert out == [a * b % q for a, b in zip(xs, ys)], "run_vector mismatch"
+    t_conv, _ = wall(lambda: dev.limbs_to_ints(dev.ints_to_limbs(xs, K_LIMBS)), 5)
+    res["run_vector_vmul_2p16_ms"] = round(t * 1e3, 2)
+    res["int_limb_roundtrip_2p16_ms"] = round(t_conv * 1e3, 2)
+    prm = find_ntt_params(BITS, N)
+    pn = K.generate_kernel(K.make_spec("ntt", BITS, 64, size=N))
+    pi = K.generate_kernel(K.make_spec("intt", BITS, 64, size=N))
+    xs = [v % prm.p for v in xs]
+    t, y = wall(lambda: K.run_ntt(pn, xs), 5)
+    assert K.run_ntt(pi, y) == xs, "run_ntt roundtrip mismatch"
+    res["run_ntt_2p16_ms"] = round(t * 1e3, 2)
+    # host-buffer BLAS (wm_blas_host), reference layout 4 x 64-bit words
+    m = 1 << 24
+    f = dev.Field(BITS, q)
+    a = canonical_random(torch, m, 61)
+    b = canonical_random(torch, m, 62)
+    ah = f.to_ref_layout(a, 64, 4).cpu().pin_memory()
+    bh = f.to_ref_layout(b, 64, 4).cpu().pin_memory()
+    oh = torch.empty_like(ah).pin_memory()
+    stream = torch.cuda.current_stream()
+    for kind in ("vmul", "axpy"):
+        call = (lambda: f.host_op("axpy", ah, bh, oh, scalar=12345)) if kind == "axpy" else \
+            (lambda: f.host_op("vmul", ah, bh, oh))
+        call()
+        torch.cuda.synchronize()
+        want = (f.axpy(12345, a, b) if kind == "axpy" else f.vmul(a, b))
+        assert torch.equal(f.from_ref_layout(oh.cuda(), 64, 4), want), f"host {kind} mismatch"
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(5):
+            call()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        res[f"host_{kind}_2p24"] = {"ms": round(ms, 3), "GB_per_s": round(3 * 32 * m / (ms * 1e-3) / 1e9, 1),
+                                    "h2d_bytes": 2 * 32 * m, "d2h_bytes": 32 * m}
+    # PCIe floor: the same bytes as plain copies (two H2D, one D2H, concurrent)
+    da, db, do = torch.empty_like(ah, device="cuda"), torch.empty_like(bh, device="cuda"), torch.empty_like(ah, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def copies():
+        s1.wait_stream(stream)
+        s2.wait_stream(stream)
+        with torch.cuda.stream(s1):
+            da.copy_(ah, non_blocking=True)
+            db.copy_(bh, non_blocking=True)
+        with torch.cuda.stream(s2):
+            oh.copy_(do, non_blocking=True)
+        stream.wait_stream(s1)
+        stream.wait_stream(s2)
+
+    copies()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(5):
+        copies()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    floor = e0.elapsed_time(e1) / 5
+    res["host_blas_pcie_floor_ms"] = round(floor, 3)
+    res["note"] = ("run_* medians of 5 wall-clock calls on Python ints (results checked); host_* through "
+                   "Field.host_op -> wm_blas_host, pinned buffers, results checked; GB/s = 3 x 32 B x n / time")
+    del a, b, ah, bh, oh, da, db, do
+    torch.cuda.empty_cache()
+    return res
 
 
 def run_four_step(args, torch, rank, world, pg):
@@ -922,6 +1019,46 @@ def cpu_baseline_subprocess(args):
         return {"value": None, "unit": UNIT, "cores": None, "kind": "unavailable", "sample": str(exc)[:200]}
 
 
+def cpu_model() -> str:
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def _bigint_ntt_job(seed: int) -> float:
+    from oracle import bigint
+    prm = bigint.find_ntt_params(BITS, N)
+    xs = bigint.uniform_residues(np.random.Generator(np.random.PCG64(seed)), N, prm["p"])
+    t0 = time.perf_counter()
+    bigint.run_ntt(xs, prm, BITS)
+    return time.perf_counter() - t0
+
+
+def run_python_bigint():
+    """The reference's Python big-integer run_ntt path (kernels.py:483-499:
+    per-butterfly Barrett mulmod/addmod/submod on Python ints), as restated
+    line for line by the oracle port (oracle/bigint.run_ntt), on one core
+    and fanned out over all host cores with multiprocessing (transforms are
+    independent; SURVEY.md §8(d) CPU baseline (i))."""
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    one = _bigint_ntt_job(1)
+    ctx = mp.get_context("fork")
+    t0 = time.perf_counter()
+    with ctx.Pool(cores) as pool:
+        pool.map(_bigint_ntt_job, range(100, 100 + cores))
+    wall = time.perf_counter() - t0
+    return {"single_process_us_per_transform": round(one * 1e6, 1),
+            "all_cores_us_per_transform": round(wall * 1e6 / cores, 1), "cores": cores,
+            "sample": f"1 transform on one core; {cores} transforms over {cores} processes (256-bit n=2^16 forward)",
+            "kind": "port", "code": "oracle/bigint.run_ntt (line-for-line restatement of the reference run_ntt "
+                                    "with its Barrett mulmod; the reference itself is not on the GPU box)"}
+
+
 def reference_arm(args, rank, world, pg):
     """--impl reference: the reference's CPU implementation of the path."""
     if rank != 0:
@@ -944,7 +1081,8 @@ def reference_arm(args, rank, world, pg):
         "config": {"workload": "256-bit forward+inverse NTT n=2^16 batch 64 (BASELINE configs[1]); --ref-transforms per step, default the whole 64+64 step",
                    "bits": BITS, "n": N, "transforms_per_step": 2 * (per_step // 2)},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": r["cores"], "kind": r["kind"],
-                         "sample": r["sample"]},
+                         "sample": r["sample"], "cpu_model": cpu_model(),
+                         "python_bigint": run_python_bigint() if args.python_bigint else None},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -970,6 +1108,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=2 * BATCH,
                     help="transforms per CPU-baseline step (default: the whole batch-64 fwd+inv step)")
     ap.add_argument("--skip-extras", action="store_true", help="only the headline workload")
+    ap.add_argument("--python-bigint", type=int, default=1,
+                    help="reference arm: also time the Python big-int run_ntt path (1/0)")
     ap.add_argument("--extras", nargs="*", default=list(EXTRAS), choices=list(EXTRAS),
                     help="which extra measurements to run (default: all)")
     ap.add_argument("--blas-bits", type=int, nargs="*", default=[128, 256, 384, 768])
@@ -1081,6 +1221,7 @@ def main():
         "reference_gpu": res["reference_gpu"],
         "full_width_bls12_381": res["full_width"],
         "steady_state_2p16": res["steady_state"],
+        "drop_in_host_boundary": res["drop_in"],
     }
     emit(out)
     if pg is not None:

@@ -208,6 +208,22 @@ int wm_ntt_twiddles(const wm_ntt_plan *p, int inverse, int64_t count, uint32_t *
 int wm_ntt_host(const wm_ntt_plan *p, int mode, int word_bits, int ref_words, const void *host_in,
                 void *host_out, int64_t batch, int64_t chunk, void *stream);
 
+/* BLAS on HOST buffers in the reference layout (`ref_words` words of
+ * `word_bits` bits per element, MSW first; kernels.to_words
+ * kernels.py:418-428): the end-to-end run_vector a reference user makes with
+ * data in host memory (kernels.py:467-480).  op: WM_OP_VADD/VSUB/VMUL/AXPY;
+ * for AXPY a_host is x, b_host is y and scalar_host the scalar (K limbs,
+ * host memory), else scalar_host is ignored.  Chunks of `chunk` elements
+ * (0 = auto) flow through an H2D / {convert, op, convert} / D2H pipeline on
+ * the field's internal streams.  out_host may equal a_host or b_host.
+ * Ordered after prior work on `stream`, which waits for the whole pipeline. */
+#define WM_OP_VADD 0
+#define WM_OP_VSUB 1
+#define WM_OP_VMUL 2
+#define WM_OP_AXPY 3
+int wm_blas_host(const wm_field *f, int op, const uint32_t *scalar_host, int word_bits, int ref_words,
+                 const void *a_host, const void *b_host, void *out_host, int64_t n, int64_t chunk, void *stream);
+
 /* ---------------------------------------------------------------- distributed four-step
  * Pieces of the multi-GPU four-step NTT (one all-to-all per transform; the
  * reference has no multi-GPU path).  See paper_2501_07535_b200/dist.py.

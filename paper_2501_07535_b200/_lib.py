@@ -19,6 +19,7 @@ WM_ECUDA = 2
 WM_EUNSUPPORTED = 3
 WM_ELENGTH = 4
 WM_NTT_FWD, WM_NTT_INV, WM_NTT_FWD_INV, WM_NTT_COPY = 0, 1, 2, 3
+WM_OP_VADD, WM_OP_VSUB, WM_OP_VMUL, WM_OP_AXPY = 0, 1, 2, 3
 WM_FIELD_KARATSUBA, WM_FIELD_MONTGOMERY, WM_FIELD_BARRETT = 1, 2, 4
 WM_REDUCTION_BARRETT, WM_REDUCTION_MONTGOMERY, WM_REDUCTION_SPECIAL_FORM = 0, 1, 2
 REDUCTION_NAMES = {WM_REDUCTION_BARRETT: "barrett", WM_REDUCTION_MONTGOMERY: "montgomery",
@@ -70,6 +71,7 @@ SIGNATURES = [
     ("wm_ntt_pass", _int, [_vp, _int, _int, _vp, _vp, _i64, _vp]),
     ("wm_ntt_twiddles", _int, [_vp, _int, _i64, _vp, _vp]),
     ("wm_ntt_host", _int, [_vp, _int, _int, _int, _vp, _vp, _i64, _i64, _vp]),
+    ("wm_blas_host", _int, [_vp, _int, _u32p, _int, _int, _vp, _vp, _vp, _i64, _i64, _vp]),
     ("wm_transpose", _int, [_int, _vp, _vp, _i64, _i64, _i64, _vp]),
     ("wm_scale_transpose", _int, [_vp, _vp, _vp, _vp, _i64, _i64, _vp]),
     ("wm_widemul", _int, [_int, _int, _vp, _vp, _vp, _i64, _vp]),

@@ -277,7 +277,10 @@ static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, 
     for (int j = 0; j < K; ++j) args.scal[j] = sh[j];
   }
   int64_t want = (n + 255) / 256;
-  int64_t cap = (int64_t)sm_count * blocks_per_sm * 4;  // a few waves' worth of resident CTAs
+#ifndef WM_BLAS_WAVES  // grid cap in waves of resident CTAs (0: one thread per element)
+#define WM_BLAS_WAVES 4
+#endif
+  int64_t cap = WM_BLAS_WAVES ? (int64_t)sm_count * blocks_per_sm * WM_BLAS_WAVES : want;
   int grid = (int)std::max<int64_t>(1, std::min(want, cap));
   blas_kernel<K, OP, STRAT><<<grid, 256, 0, st>>>(a, b, out, n, args);
   WM_LAUNCH_CHECK("blas_kernel launch");
@@ -628,6 +631,7 @@ int wm_field_reduction(const wm_field *f) {
 }
 
 int wm_field_destroy(wm_field *f) {
+  if (f) f->host.release();
   delete f;
   return WM_OK;
 }

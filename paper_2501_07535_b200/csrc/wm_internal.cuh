@@ -74,6 +74,27 @@ Big big_shl_mod(const Big &a, int e, const Big &q);
 // Montgomery form a * 2^(32K) mod q.
 inline Big to_mont(const Big &a, const Big &q) { return big_shl_mod(a, 32 * (int)q.size(), q); }
 
+// ------------------------------------------------------------------ host pipeline
+// Streams, events and device staging slots of a host-buffer pipeline
+// (wm_ntt_host, wm_blas_host): h2d, d2h, then kComp compute streams; chunks
+// round-robin over the compute streams and over kSlots staging slots.
+// Created on first use, guarded by `mu` (one pipelined call at a time per
+// owner object).
+struct HostPipe {
+  static constexpr int kComp = 4;
+  static constexpr int kStreams = 2 + kComp;
+  static constexpr int kSlots = 8;
+  std::mutex mu;
+  bool ready = false;
+  cudaStream_t hs[kStreams] = {};
+  cudaEvent_t ev_in[kSlots] = {}, ev_comp[kSlots] = {}, ev_out[kSlots] = {};
+  cudaEvent_t ev_entry = nullptr, ev_done = nullptr;
+  void *slot_mem[kSlots] = {};
+  int64_t slot_bytes = 0;
+  int ensure(int64_t bytes);  // streams/events created, every slot >= bytes
+  void release();
+};
+
 // ------------------------------------------------------------------ objects
 }  // namespace wm
 
@@ -92,6 +113,7 @@ struct wm_field {
   bool pm = false;
   uint32_t pm_c = 0;
   int pm_sh = 0;
+  wm::HostPipe host;  // wm_blas_host staging (created on first use)
 };
 
 struct wm_pass_plan {
@@ -135,18 +157,7 @@ struct wm_ntt_plan {
   cudaEvent_t ws_ev = nullptr;
   void *ws = nullptr;
   int64_t ws_bytes = 0;
-  // host pipeline (wm_ntt_host): internal streams, events and staging slots
-  std::mutex host_mu;
-  bool host_ready = false;
-  // h2d, d2h, then kComp compute streams: chunks round-robin over the compute
-  // streams so the kernels of consecutive (small) chunks share the GPU
-  static constexpr int kComp = 4;
-  static constexpr int kStreams = 2 + kComp;
-  cudaStream_t hs[kStreams] = {};
-  static constexpr int kSlots = 8;
-  cudaEvent_t ev_in[kSlots], ev_comp[kSlots], ev_out[kSlots], ev_entry = nullptr, ev_done = nullptr;
-  void *slot_mem[kSlots] = {};
-  int64_t slot_bytes = 0;
+  wm::HostPipe host;  // wm_ntt_host staging (created on first use)
 };
 
 namespace wm {
@@ -176,5 +187,5 @@ void preload_ntt(const wm_field *f);
 void preload_field(const wm_field *f);
 int ntt_run_internal(const wm_ntt_plan *p, bool inverse, const uint32_t *in, uint32_t *out, int64_t batch,
                      void *workspace, cudaStream_t st, const uint32_t *mul_by = nullptr);
-int release_host_pipeline(wm_ntt_plan *p);
+
 }  // namespace wm

@@ -44,8 +44,11 @@ WM_DEV void ld8_stream(uint32_t *r, const uint32_t *p) {
 #ifndef WM_LD_L1_MULTI
 #define WM_LD_L1_MULTI 1  // A/B: 384-bit vadd 5.74 -> 6.40 TB/s (profiles/r01_ab_l1_multi_access.txt)
 #endif
+#ifndef WM_LD_STREAM  // 0: every element load through L1 (__ldg), for A/B runs
+#define WM_LD_STREAM 1
+#endif
 template <int K>
-constexpr bool kStreamLd = !(WM_LD_L1_MULTI && (K / VecWidth<K>::V) > 1);
+constexpr bool kStreamLd = WM_LD_STREAM && !(WM_LD_L1_MULTI && (K / VecWidth<K>::V) > 1);
 
 // Load element i (K limbs) from global memory.
 template <int K>

@@ -248,7 +248,7 @@ int wm_ntt_plan_destroy(wm_ntt_plan *p) {
   if (p->tw_fwd || p->tw_inv || p->tw_inv_scaled || p->tw_img) cudaStreamSynchronize(cudaStreamLegacy);
   if (p->ws) cudaFree(p->ws);
   if (p->ws_ev) cudaEventDestroy(p->ws_ev);
-  release_host_pipeline(p);
+  p->host.release();
   delete p;
   return WM_OK;
 }

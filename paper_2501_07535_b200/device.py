@@ -201,6 +201,37 @@ class Field:
         _lib.check(self.lib.wm_axpy(self._h, sl, _ptr(x), _ptr(y), _ptr(out), n, _stream_ptr(stream)))
         return out
 
+    def host_op(self, kind: str, a_host, b_host, out_host, scalar: int = 0, word_bits: int = 64,
+                ref_words: int | None = None, chunk: int = 0, stream=None):
+        """End-to-end BLAS on HOST tensors in the reference layout (AoS,
+        MSW-first words, kernels.to_words): out = a (+,-,*) b, or
+        out = scalar*a + b for "axpy", through the pipelined C ABI call
+        ``wm_blas_host`` (chunked H2D / convert + kernel + convert / D2H on
+        overlapping streams).  Pinned host tensors give full PCIe overlap."""
+        codes = {"vadd": _lib.WM_OP_VADD, "vsub": _lib.WM_OP_VSUB, "vmul": _lib.WM_OP_VMUL,
+                 "axpy": _lib.WM_OP_AXPY}
+        if kind not in codes:
+            raise ValueError(f"bad kind {kind!r}")
+        if ref_words is None:
+            ref_words = -(-self.bits // word_bits)
+            ref_words = 1 << (ref_words - 1).bit_length()  # reference pads to a power of two
+        per = ref_words * word_bits // 8
+        for t in (a_host, b_host, out_host):
+            if t.is_cuda or not t.is_contiguous():
+                raise ValueError("host_op takes contiguous host tensors")
+        nbytes = a_host.numel() * a_host.element_size()
+        if nbytes % per or any(t.numel() * t.element_size() != nbytes for t in (b_host, out_host)):
+            raise ValueError("host buffers differ in size or are not whole elements")
+        sl = None
+        if kind == "axpy":
+            if not 0 <= int(scalar) < self.q:
+                raise ValueError("axpy scalar must be a canonical residue (0 <= a < q)")
+            sl = _lib.u32_array(ints_to_limbs([int(scalar)], self.limbs)[0].tolist())
+        _lib.check(self.lib.wm_blas_host(self._h, codes[kind], sl, word_bits, ref_words, a_host.data_ptr(),
+                                         b_host.data_ptr(), out_host.data_ptr(), nbytes // per, chunk,
+                                         _stream_ptr(stream)), "wm_blas_host")
+        return out_host
+
     # ---------------------------------------------------------------- layout
     def from_ref_layout(self, ref, word_bits: int, ref_words: int, out=None, stream=None):
         """Reference AoS MSW-first words (kernels.to_words) -> limb tensor."""
