@@ -248,6 +248,23 @@ int wm_scale_transpose_scatter(const wm_field *f, const uint32_t *in, const uint
 int wm_twiddle_table_2d(const wm_field *f, int64_t n, const uint32_t *root_host, int64_t row0,
                         int64_t rows, int64_t cols, uint32_t *table, void *stream);
 
+/* Factored twiddles for the four-step: root^e = hi[e >> logB] * lo[e mod 2^logB]
+ * (e < n), two tables of 2^logB and n / 2^logB entries of K words (in the
+ * field's product form: Montgomery form for full-width fields) — O(sqrt n)
+ * memory instead of wm_twiddle_table_2d's rows x cols Shoup pairs.
+ *   wm_twiddle_factors:    fill lo[0 .. 2^logB) and hi[0 .. n/2^logB).
+ *   wm_scale_transpose_fx: out[c][r] = in[r][c] * root^((row0 + r) c mod n)
+ *     (canonical).  P == 0: into `out` ([cols][rows]).  P >= 1: output row
+ *     c goes to dst_ptrs[c / (cols/P)] — layout 0 at [src_rank][c mod cols/P]
+ *     [rows] (an all-to-all's block layout), layout 1 at [c mod cols/P]
+ *     [src_rank * rows + r] (the receiving rank's phase-2 rows: no block
+ *     transpose needed). */
+int wm_twiddle_factors(const wm_field *f, int64_t n, const uint32_t *root_host, int logB, uint32_t *lo,
+                       uint32_t *hi, void *stream);
+int wm_scale_transpose_fx(const wm_field *f, const uint32_t *in, const uint32_t *lo, const uint32_t *hi, int logB,
+                          int64_t n, int64_t row0, uint32_t *out, const uint64_t *dst_ptrs, int P, int src_rank,
+                          int layout, int64_t rows, int64_t cols, void *stream);
+
 /* ---------------------------------------------------------------- diagnostics
  * Roofline inputs for the integer-bound kernels (bench.py).
  *   wm_probe_imad_wide: launch a kernel of 8 independent 32x32->64 product

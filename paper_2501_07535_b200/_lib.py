@@ -77,6 +77,9 @@ SIGNATURES = [
     ("wm_widemul", _int, [_int, _int, _vp, _vp, _vp, _i64, _vp]),
     ("wm_scale_transpose_scatter", _int, [_vp, _vp, _vp, _vp, ctypes.c_int, ctypes.c_int, _i64, _i64, _vp]),
     ("wm_twiddle_table_2d", _int, [_vp, _i64, _u32p, _i64, _i64, _i64, _vp, _vp]),
+    ("wm_twiddle_factors", _int, [_vp, _i64, _u32p, _int, _vp, _vp, _vp]),
+    ("wm_scale_transpose_fx", _int, [_vp, _vp, _vp, _vp, _int, _i64, _i64, _vp, _vp, _int, _int, _int, _i64, _i64,
+                                     _vp]),
     ("wm_probe_imad_wide", _int, [_int, _i64, _vp, _vp, ctypes.POINTER(_i64)]),
     ("wm_ntt_pass_work", _int, [_vp, _int, _int, _i64, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double)]),
     ("wm_ref_to_limbs", _int, [_int, _int, _int, _vp, _vp, _i64, _vp]),

@@ -203,6 +203,169 @@ __global__ void twiddle_2d_kernel(uint32_t *table, int64_t n, int64_t row0, int6
 }
 
 
+// ------------------------------------------------------------------ factored twiddles
+// root^e = hi[e >> logB] * lo[e & (2^logB - 1)] for e < n: two tables of
+// 2^logB and n / 2^logB entries (K words each, in the field's product form:
+// Montgomery form for full-width fields) replace the materialised
+// rows x cols table of Shoup pairs; each twiddle costs one more product.
+// At n = 2^24, logB = 12: 2 x 4096 entries (256 KiB at 256 bits) instead of
+// 2^24 / P pairs (1 GiB / P).
+enum { kDistBarrett = 0, kDistMont = 1, kDistPm = 3 };
+
+template <int K, int MODE>
+WM_DEV void dist_twiddle_mul(uint32_t (&res)[K], const uint32_t (&v)[K], const uint32_t (&lo)[K],
+                             const uint32_t (&hi)[K], const FieldConst<K> &F) {
+  uint32_t w[K];
+  if constexpr (MODE == kDistPm) {
+    mul_pm_lazy<K>(w, hi, lo, F.pm_c, F.pm_sh);   // w < 2q
+    mul_pm_lazy<K>(res, w, v, F.pm_c, F.pm_sh);   // < 2^m + 2^68
+    cond_sub<K>(res, F.q);
+  } else if constexpr (MODE == kDistMont) {
+    mont_mul<K>(w, hi, lo, F.q, F.qinv);  // (hi lo) R
+    mont_mul<K>(res, v, w, F.q, F.qinv);
+  } else {
+    mul_barrett<K>(w, hi, lo, F);
+    mul_barrett<K>(res, v, w, F);
+  }
+}
+
+struct FxArgs {
+  int64_t n;     // transform length (exponents mod n)
+  int64_t row0;  // global index of local row 0
+  int logB;      // lo table covers exponents < 2^logB
+  int layout;    // scatter layout: 0 [src][c_local][rows], 1 [c_local][P * rows] (rows of the next phase)
+};
+
+// out[c][r] = in[r][c] * root^((row0 + r) c mod n), canonical, twiddles from
+// the factor tables.  With a ScatterDst, output row c goes to rank
+// d = c / cpr: layout 0 at [src][c mod cpr][r] (the block layout of an
+// all-to-all), layout 1 at [c mod cpr][src * rows + r] — already the
+// receiving rank's phase-2 rows, so no block transpose follows.
+template <int K, int MODE>
+__global__ void __launch_bounds__(256) scale_transpose_fx_kernel(const uint32_t *in, const uint32_t *lo_t,
+                                                                 const uint32_t *hi_t, uint32_t *out, int64_t rows,
+                                                                 int64_t cols, const __grid_constant__ FieldConst<K> F,
+                                                                 const __grid_constant__ ScatterDst D,
+                                                                 const FxArgs A) {
+  extern __shared__ uint32_t tile[];  // TT * (TT*K + 1)
+  const int64_t r0 = (int64_t)blockIdx.y * TT, c0 = (int64_t)blockIdx.x * TT;
+  const int stride = TT * K + 1;
+  const uint64_t nmask = (uint64_t)A.n - 1, lmask = ((uint64_t)1 << A.logB) - 1;
+  for (int idx = threadIdx.x; idx < TT * TT; idx += blockDim.x) {
+    const int rr = idx / TT, cc = idx - rr * TT;
+    const int64_t r = r0 + rr, c = c0 + cc;
+    if (r < rows && c < cols) {
+      const uint64_t e = ((uint64_t)(A.row0 + r) * (uint64_t)c) & nmask;
+      uint32_t v[K], lo[K], hi[K], res[K];
+      ldg_elem<K>(v, in + (r * cols + c) * K);
+      ldg_elem<K>(lo, lo_t + (e & lmask) * K);
+      ldg_elem<K>(hi, hi_t + (e >> A.logB) * K);
+      dist_twiddle_mul<K, MODE>(res, v, lo, hi, F);
+#pragma unroll
+      for (int j = 0; j < K; ++j) tile[rr * stride + cc * K + j] = res[j];
+    }
+  }
+  __syncthreads();
+  for (int idx = threadIdx.x; idx < TT * TT * K; idx += blockDim.x) {
+    const int cc = idx / (TT * K), w = idx - cc * (TT * K);
+    const int rr = w / K, ww = w - rr * K;
+    const int64_t c = c0 + cc, r = r0 + rr;
+    if (r < rows && c < cols) {
+      uint32_t *row_base;
+      if (D.P > 0) {
+        const int64_t d = c / D.cpr, cl = c - d * D.cpr;
+        uint32_t *dst = reinterpret_cast<uint32_t *>(D.ptr[d]);
+        row_base = A.layout == 0 ? dst + ((int64_t)D.src * D.cpr + cl) * rows * K
+                                 : dst + (cl * D.P + D.src) * rows * K;
+      } else {
+        row_base = out + c * rows * K;
+      }
+      row_base[r0 * K + w] = tile[rr * stride + cc * K + ww];
+    }
+  }
+}
+
+// table[i] = root^(i * step) for i < count (product form; MONT: root and one
+// arrive in Montgomery form).  Setup only.
+template <int K, bool MONT>
+__global__ void twiddle_factor_kernel(uint32_t *table, int64_t count, int64_t step, int64_t n,
+                                      const __grid_constant__ FieldConst<K> F, const __grid_constant__ Limbs<K> root,
+                                      const __grid_constant__ Limbs<K> one) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  uint32_t b[K], x[K], tmp[K];
+  copy_n<K>(b, root.v);
+  copy_n<K>(x, one.v);
+  for (uint64_t e = ((uint64_t)i * (uint64_t)step) & (uint64_t)(n - 1); e; e >>= 1) {
+    if (e & 1) {
+      dist_mul<K, MONT>(tmp, x, b, F);
+      copy_n<K>(x, tmp);
+    }
+    dist_mul<K, MONT>(tmp, b, b, F);
+    copy_n<K>(b, tmp);
+  }
+  stg_elem<K>(table + i * K, x);
+}
+
+template <int K, int MODE>
+static int launch_fx_t(const wm_field *f, const uint32_t *in, const uint32_t *lo, const uint32_t *hi, uint32_t *out,
+                       int64_t rows, int64_t cols, cudaStream_t st, const ScatterDst &D, const FxArgs &A) {
+  const size_t smem = (size_t)TT * (TT * K + 1) * 4;
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr)) {
+    WM_CUDA_TRY(cudaFuncSetAttribute(scale_transpose_fx_kernel<K, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)std::max<size_t>(smem, 48 * 1024)));
+  }
+  dim3 grid((unsigned)((cols + TT - 1) / TT), (unsigned)((rows + TT - 1) / TT));
+  scale_transpose_fx_kernel<K, MODE><<<grid, 256, smem, st>>>(in, lo, hi, out, rows, cols, field_const<K>(f), D, A);
+  WM_LAUNCH_CHECK("scale_transpose_fx launch");
+  return WM_OK;
+}
+
+template <int K>
+static int launch_fx(const wm_field *f, const uint32_t *in, const uint32_t *lo, const uint32_t *hi, uint32_t *out,
+                     int64_t rows, int64_t cols, cudaStream_t st, const ScatterDst &D, const FxArgs &A) {
+  if (f->mont) {
+    if constexpr (dist_mont_built<K>()) return launch_fx_t<K, kDistMont>(f, in, lo, hi, out, rows, cols, st, D, A);
+    return fail(WM_EUNSUPPORTED, "limb count not built into the full-width kernels");
+  }
+  if constexpr (K >= 3) {
+    if (f->pm) return launch_fx_t<K, kDistPm>(f, in, lo, hi, out, rows, cols, st, D, A);
+  }
+  return launch_fx_t<K, kDistBarrett>(f, in, lo, hi, out, rows, cols, st, D, A);
+}
+
+template <int K>
+static int launch_twiddle_factors(const wm_field *f, int64_t n, const uint32_t *root, int logB, uint32_t *lo,
+                                  uint32_t *hi, cudaStream_t st) {
+  Big r(root, root + K), one(K, 0u);
+  one[0] = 1;
+  if (f->mont) {
+    r = to_mont(r, f->q);
+    one = to_mont(one, f->q);
+  }
+  Limbs<K> rt, on;
+  for (int j = 0; j < K; ++j) {
+    rt.v[j] = r[j];
+    on.v[j] = one[j];
+  }
+  const int64_t nlo = (int64_t)1 << logB, nhi = n >> logB;
+  const FieldConst<K> F = field_const<K>(f);
+  if (f->mont) {
+    if constexpr (dist_mont_built<K>()) {
+      twiddle_factor_kernel<K, true><<<(unsigned)((nlo + 127) / 128), 128, 0, st>>>(lo, nlo, 1, n, F, rt, on);
+      twiddle_factor_kernel<K, true><<<(unsigned)((nhi + 127) / 128), 128, 0, st>>>(hi, nhi, nlo, n, F, rt, on);
+      WM_LAUNCH_CHECK("twiddle_factor launch");
+      return WM_OK;
+    }
+    return fail(WM_EUNSUPPORTED, "limb count not built into the full-width kernels");
+  }
+  twiddle_factor_kernel<K, false><<<(unsigned)((nlo + 127) / 128), 128, 0, st>>>(lo, nlo, 1, n, F, rt, on);
+  twiddle_factor_kernel<K, false><<<(unsigned)((nhi + 127) / 128), 128, 0, st>>>(hi, nhi, nlo, n, F, rt, on);
+  WM_LAUNCH_CHECK("twiddle_factor launch");
+  return WM_OK;
+}
+
 template <int K, bool MONT>
 static int launch_scale_transpose_t(const wm_field *f, const uint32_t *in, const uint32_t *table, uint32_t *out,
                                     int64_t rows, int64_t cols, cudaStream_t st, const ScatterDst &D) {
@@ -331,6 +494,63 @@ int wm_scale_transpose_scatter(const wm_field *f, const uint32_t *in, const uint
 #define WM_CASE(k) \
   case k:          \
     return launch_scale_transpose<k>(f, in, table, nullptr, rows, cols, st, D);
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      return fail(WM_EUNSUPPORTED, "limb count not built in");
+  }
+}
+
+int wm_twiddle_factors(const wm_field *f, int64_t n, const uint32_t *root_host, int logB, uint32_t *lo,
+                       uint32_t *hi, void *stream) {
+  if (!f || !root_host || !lo || !hi) return fail(WM_EINVAL, "null argument");
+  if (n < 2 || (n & (n - 1))) return fail(WM_EINVAL, "n must be a power of two >= 2");
+  if (logB < 0 || ((int64_t)1 << logB) > n) return fail(WM_EINVAL, "logB outside [0, log2 n]");
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (f->K) {
+#define WM_CASE(k) \
+  case k:          \
+    return launch_twiddle_factors<k>(f, n, root_host, logB, lo, hi, st);
+    WM_NTT_KS(WM_CASE)
+#undef WM_CASE
+    default:
+      return fail(WM_EUNSUPPORTED, "limb count not built in");
+  }
+}
+
+int wm_scale_transpose_fx(const wm_field *f, const uint32_t *in, const uint32_t *lo, const uint32_t *hi, int logB,
+                          int64_t n, int64_t row0, uint32_t *out, const uint64_t *dst_ptrs, int P, int src_rank,
+                          int layout, int64_t rows, int64_t cols, void *stream) {
+  if (!f) return fail(WM_EINVAL, "null field");
+  if (rows < 0 || cols < 0 || row0 < 0) return fail(WM_EINVAL, "bad shape");
+  if (n < 2 || (n & (n - 1))) return fail(WM_EINVAL, "n must be a power of two >= 2");
+  if (logB < 0 || ((int64_t)1 << logB) > n) return fail(WM_EINVAL, "logB outside [0, log2 n]");
+  if (P < 0 || P > kMaxPeers) return fail(WM_EUNSUPPORTED, "peer count outside 0..16");
+  if (layout != 0 && layout != 1) return fail(WM_EINVAL, "layout must be 0 or 1");
+  if (rows == 0 || cols == 0) return WM_OK;
+  if (!in || !lo || !hi) return fail(WM_EINVAL, "null pointer");
+  ScatterDst D{};
+  if (P == 0) {
+    if (!out || out == in) return fail(WM_EINVAL, "bad output (in/out must differ)");
+  } else {
+    if (src_rank < 0 || src_rank >= P) return fail(WM_EINVAL, "source rank outside 0..P-1");
+    if (cols % P) return fail(WM_EINVAL, "P must divide cols");
+    if (!dst_ptrs) return fail(WM_EINVAL, "null destination array");
+    for (int d = 0; d < P; ++d) {
+      if (!dst_ptrs[d]) return fail(WM_EINVAL, "null destination pointer");
+      if (dst_ptrs[d] == (uint64_t)(uintptr_t)in) return fail(WM_EINVAL, "destination aliases the input");
+      D.ptr[d] = dst_ptrs[d];
+    }
+    D.P = P;
+    D.src = src_rank;
+    D.cpr = cols / P;
+  }
+  FxArgs A{n, row0, logB, layout};
+  cudaStream_t st = (cudaStream_t)stream;
+  switch (f->K) {
+#define WM_CASE(k) \
+  case k:          \
+    return launch_fx<k>(f, in, lo, hi, out, rows, cols, st, D, A);
     WM_NTT_KS(WM_CASE)
 #undef WM_CASE
     default:

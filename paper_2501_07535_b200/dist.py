@@ -8,9 +8,12 @@
 
       rank r holds rows j1 in its block (N1/P rows), row j1 = x[j1 + N1 j2]
       (a) N2-point row NTTs                        wm_ntt_forward
-      (b) * root^(j1 k2), transpose to [k2][j1]    wm_scale_transpose (fused)
+      (b) * root^(j1 k2), transpose to [k2][j1]    wm_scale_transpose_fx (twiddles from two
+                                                   O(sqrt n) factor tables, fused)
       (c) all-to-all of the P column blocks        torch.distributed (NCCL)
       (d) [P][N2/P][N1/P] -> [N2/P][N1]            wm_transpose (block transpose)
+      (fused exchange: (b)+(c)+(d) are one kernel storing rank d's phase-2
+       rows straight into its symmetric-memory receive buffer, SymmComm)
       (e) N1-point row NTTs                        wm_ntt_forward
       rank r now holds rows k2 in its block, row k2 = y[k2 + N2 k1]
 
@@ -214,15 +217,26 @@ class DeviceBackend:
         lib = self.field.lib
         enc = lambda v: _lib.u32_array(ints_to_limbs([v], K)[0].tolist())  # noqa: E731
         stream = torch.cuda.current_stream().cuda_stream
-        rows_f, rows_i = n1 // P, n2 // P
-        self.tw_fwd = torch.empty((rows_f, n2, 2 * K), dtype=torch.int32, device="cuda")
-        _lib.check(lib.wm_twiddle_table_2d(self.field.handle, n, enc(w), rank * rows_f, rows_f, n2,
-                                           self.tw_fwd.data_ptr(), stream), "wm_twiddle_table_2d")
-        self.tw_inv = torch.empty((rows_i, n1, 2 * K), dtype=torch.int32, device="cuda")
-        _lib.check(lib.wm_twiddle_table_2d(self.field.handle, n, enc(wi), rank * rows_i, rows_i, n1,
-                                           self.tw_inv.data_ptr(), stream), "wm_twiddle_table_2d")
+        # inter-rank twiddles root^(j1 k2) from two factor tables of O(sqrt n)
+        # entries (wm_twiddle_factors): 2 x 2^12 entries at n = 2^24
+        logn = n.bit_length() - 1
+        self.logB = (logn + 1) // 2
+        self.rows_f, self.rows_i = n1 // P, n2 // P
+        self.row0_f, self.row0_i = rank * self.rows_f, rank * self.rows_i
+        self.tw = {}
+        for inv, root in ((False, w), (True, wi)):
+            lo = torch.empty((1 << self.logB, K), dtype=torch.int32, device="cuda")
+            hi = torch.empty((n >> self.logB, K), dtype=torch.int32, device="cuda")
+            _lib.check(lib.wm_twiddle_factors(self.field.handle, n, enc(root), self.logB, lo.data_ptr(),
+                                              hi.data_ptr(), stream), "wm_twiddle_factors")
+            self.tw[inv] = (lo, hi)
+        self.n = n
         self.lib = lib
         self._lib = _lib
+
+    def table_bytes(self) -> int:
+        """Device bytes of the inter-rank twiddle tables (both directions)."""
+        return sum(t.numel() * t.element_size() for pair in self.tw.values() for t in pair)
 
     def empty(self, shape):
         return self.torch.empty(tuple(shape) + (self.K,), dtype=self.torch.int32, device="cuda")
@@ -231,28 +245,32 @@ class DeviceBackend:
         plan = self.plan_n2 if length == self.layout.n2 else self.plan_n1
         return plan.inverse(x) if inverse else plan.forward(x)
 
-    def scale_transpose(self, x, inverse: bool):
+    def _fx(self, x, inverse: bool, out=None, dst_ptrs=None, src_rank: int = 0, layout: int = 1):
+        import ctypes
         rows, cols = x.shape[0], x.shape[1]
-        out = self.empty((cols, rows))
-        table = self.tw_inv if inverse else self.tw_fwd
+        lo, hi = self.tw[inverse]
+        row0 = self.row0_i if inverse else self.row0_f
+        P = 0 if dst_ptrs is None else len(dst_ptrs)
+        arr = None if dst_ptrs is None else (ctypes.c_uint64 * P)(*[int(p) for p in dst_ptrs])
         stream = self.torch.cuda.current_stream().cuda_stream
-        self._lib.check(self.lib.wm_scale_transpose(self.field.handle, x.data_ptr(), table.data_ptr(),
-                                                    out.data_ptr(), rows, cols, stream), "wm_scale_transpose")
+        self._lib.check(self.lib.wm_scale_transpose_fx(self.field.handle, x.data_ptr(), lo.data_ptr(), hi.data_ptr(),
+                                                       self.logB, self.n, row0,
+                                                       out.data_ptr() if out is not None else None, arr, P, src_rank,
+                                                       layout, rows, cols, stream), "wm_scale_transpose_fx")
+
+    def scale_transpose(self, x, inverse: bool):
+        """[rows][cols] -> [cols][rows] times root^((row0 + r) c) (wm_scale_transpose_fx)."""
+        out = self.empty((x.shape[1], x.shape[0]))
+        self._fx(x, inverse, out=out)
         return out
 
-    def scale_transpose_scatter(self, x, inverse: bool, dst_ptrs, src_rank: int):
+    def scale_transpose_scatter(self, x, inverse: bool, dst_ptrs, src_rank: int, layout: int = 1):
         """scale_transpose with the all-to-all fused in: column block d of the
         transposed output goes straight into dst_ptrs[d] (rank d's receive
-        buffer, [P][cols/P][rows] elements) at source slot `src_rank`."""
-        rows, cols = x.shape[0], x.shape[1]
-        table = self.tw_inv if inverse else self.tw_fwd
-        P = len(dst_ptrs)
-        import ctypes
-        arr = (ctypes.c_uint64 * P)(*[int(p) for p in dst_ptrs])
-        stream = self.torch.cuda.current_stream().cuda_stream
-        self._lib.check(self.lib.wm_scale_transpose_scatter(self.field.handle, x.data_ptr(), table.data_ptr(), arr,
-                                                            P, src_rank, rows, cols, stream),
-                        "wm_scale_transpose_scatter")
+        buffer).  layout 1 stores it as rank d's phase-2 rows
+        ([cols/P][P * rows]: no block transpose after the exchange); layout 0
+        as an all-to-all's blocks ([P][cols/P][rows])."""
+        self._fx(x, inverse, dst_ptrs=dst_ptrs, src_rank=src_rank, layout=layout)
 
     def block_transpose(self, x, rows: int, cols: int, block: int):
         """[rows][cols][block] -> [cols][rows][block] (block = elements)."""
@@ -283,13 +301,17 @@ class FourStepNtt:
         return self.backend.scale_transpose(y, inverse)  # [row_len][rows_local]
 
     # phase 2: received [P][row_len/P][rows_local] -> block transpose -> row transforms
-    def phase2(self, d, inverse: bool):
+    # (rows=True: received already as rows [row_len/P][other], fused layout 1)
+    def phase2(self, d, inverse: bool, rows: bool = False):
         L = self.layout
         P = self.world
         row_len = L.n1 if inverse else L.n2      # length of the phase-1 rows
         other = L.n2 if inverse else L.n1        # length of the phase-2 rows
         rows_local = other // P
-        e = self.backend.block_transpose(d, P, row_len // P, rows_local)  # [row_len/P][other]
+        if rows:
+            e = d.reshape(row_len // P, other, -1)
+        else:
+            e = self.backend.block_transpose(d, P, row_len // P, rows_local)  # [row_len/P][other]
         return self.backend.row_ntt(e, other, inverse)
 
     def _run(self, x, inverse: bool):
@@ -312,10 +334,10 @@ class FourStepNtt:
         k = self.backend.K
         words = row_len * (other // P) * k
         self.comm.barrier()  # every peer is done reading its receive buffer
-        self.backend.scale_transpose_scatter(y, inverse, self.comm.peer_ptrs, self.rank)
-        self.comm.barrier()  # every block has landed
-        d = self.comm.recv[:words].view(row_len, other // P, k)
-        return self.phase2(d, inverse)
+        self.backend.scale_transpose_scatter(y, inverse, self.comm.peer_ptrs, self.rank, layout=1)
+        self.comm.barrier()  # every block has landed, as this rank's phase-2 rows
+        d = self.comm.recv[:words].view(row_len // P, other, k)
+        return self.phase2(d, inverse, rows=True)
 
     def forward(self, x):
         """x: [N1/P, N2, K] local rows -> [N2/P, N1, K] (rows k2 of y)."""
@@ -336,12 +358,12 @@ def loopback_transform_fused(engines, xs, inverse: bool = False):
     row_len = L.n1 if inverse else L.n2
     other = L.n2 if inverse else L.n1
     k = engines[0].backend.K
-    recvs = [torch.empty((row_len, other // P, k), dtype=torch.int32, device="cuda") for _ in range(P)]
+    recvs = [torch.empty((row_len // P, other, k), dtype=torch.int32, device="cuda") for _ in range(P)]
     ptrs = [r.data_ptr() for r in recvs]
     for r, (e, x) in enumerate(zip(engines, xs)):
         y = e.backend.row_ntt(x, row_len, inverse)
-        e.backend.scale_transpose_scatter(y, inverse, ptrs, r)
-    return [e.phase2(d, inverse) for e, d in zip(engines, recvs)]
+        e.backend.scale_transpose_scatter(y, inverse, ptrs, r, layout=1)
+    return [e.phase2(d, inverse, rows=True) for e, d in zip(engines, recvs)]
 
 
 def loopback_transform(engines, xs, inverse: bool = False):

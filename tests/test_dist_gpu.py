@@ -208,3 +208,58 @@ def test_loopback_2p24_roundtrip_and_points(cuda):
     pts = OracleField(prm.p, 256).ntt_points(x.cpu().numpy().view(np.uint32), prm.root, ks)
     for i, k in enumerate(ks):
         assert np.array_equal(y[k].view(np.uint32), pts[i])
+
+
+@pytest.mark.parametrize("bits,strategy,logn", [(256, "schoolbook", 12), (256, "barrett", 12), (384, "schoolbook", 11),
+                                                (256, "montgomery", 12), (128, "schoolbook", 13)])
+def test_factored_twiddles_scale_transpose(cuda, bits, strategy, logn):
+    """wm_twiddle_factors + wm_scale_transpose_fx: root^((row0 + r) c) from two
+    O(sqrt n) factor tables, times the data, transposed — against Python ints,
+    for special-form, Barrett and Montgomery fields; and the fused scatter in
+    both layouts (layout 1 = the receiving rank's phase-2 rows)."""
+    import torch
+    from paper_2501_07535_b200 import _lib
+    from paper_2501_07535_b200 import device as dev
+    from paper_2501_07535_b200.params import NttParams, find_ntt_params
+    lib = _lib.load()
+    n = 1 << logn
+    if strategy == "montgomery":
+        p = 0x73EDA753299D7D483339D80809A1D80553BDA402FFFE5BFEFFFFFFFF00000001
+        w = pow(7, (p - 1) // n, p)
+        prm = NttParams(n=n, p=p, root=w, root_inv=pow(w, -1, p), n_inv=pow(n, -1, p))
+        f = dev.Field(bits, p, "montgomery")
+    else:
+        prm = find_ntt_params(bits, n)
+        f = dev.Field(bits, prm.p, reduction="barrett" if strategy == "barrett" else "auto")
+    K = f.limbs
+    logB = (logn + 1) // 2
+    lo = torch.empty((1 << logB, K), dtype=torch.int32, device="cuda")
+    hi = torch.empty((n >> logB, K), dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    root = _lib.u32_array(dev.ints_to_limbs([prm.root], K)[0].tolist())
+    _lib.check(lib.wm_twiddle_factors(f.handle, n, root, logB, lo.data_ptr(), hi.data_ptr(), st))
+    rows, cols, row0, P = 24, 40, 17, 4
+    rnd = random.Random(logn + bits)
+    xs = [rnd.randrange(prm.p) for _ in range(rows * cols)]
+    xs[:cols] = [prm.p - 1] * cols
+    x = dev.to_device(dev.ints_to_limbs(xs, K)).reshape(rows, cols, K)
+    want = [xs[r * cols + c] * pow(prm.root, ((row0 + r) * c) % n, prm.p) % prm.p
+            for c in range(cols) for r in range(rows)]
+    out = torch.empty((cols, rows, K), dtype=torch.int32, device="cuda")
+    _lib.check(lib.wm_scale_transpose_fx(f.handle, x.data_ptr(), lo.data_ptr(), hi.data_ptr(), logB, n, row0,
+                                         out.data_ptr(), None, 0, 0, 0, rows, cols, st))
+    assert dev.limbs_to_ints(dev.to_host(out).reshape(-1, K)) == want
+    import ctypes
+    for layout in (0, 1):
+        recv = [torch.zeros((P, cols // P, rows, K), dtype=torch.int32, device="cuda") for _ in range(P)]
+        arr = (ctypes.c_uint64 * P)(*[t.data_ptr() for t in recv])
+        src = 2
+        _lib.check(lib.wm_scale_transpose_fx(f.handle, x.data_ptr(), lo.data_ptr(), hi.data_ptr(), logB, n, row0,
+                                             None, arr, P, src, layout, rows, cols, st))
+        for d in range(P):
+            block = out[d * (cols // P):(d + 1) * (cols // P)]  # [cols/P][rows][K]
+            if layout == 0:
+                assert torch.equal(recv[d][src], block)
+            else:  # [cols/P][P * rows]: source src's rows at columns src*rows ..
+                got = recv[d].reshape(cols // P, P, rows, K)[:, src]
+                assert torch.equal(got, block)
