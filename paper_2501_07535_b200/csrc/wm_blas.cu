@@ -280,7 +280,12 @@ static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, 
 #ifndef WM_BLAS_WAVES  // grid cap in waves of resident CTAs (0: one thread per element)
 #define WM_BLAS_WAVES 4
 #endif
-  int64_t cap = WM_BLAS_WAVES ? (int64_t)sm_count * blocks_per_sm * WM_BLAS_WAVES : want;
+  // light kernels (<= 4 limbs, add/sub) keep one thread per element: more
+  // loads in flight (128-bit vmul/axpy 6.05 -> 6.52 TB/s); heavier ones run
+  // a few waves of grid-stride CTAs (256-bit axpy 5.55 -> 5.87 TB/s),
+  // profiles/r02_ab_blas_grid.txt
+  const bool light = K <= 4 || OP == OP_VADD || OP == OP_VSUB;
+  int64_t cap = (WM_BLAS_WAVES && !light) ? (int64_t)sm_count * blocks_per_sm * WM_BLAS_WAVES : want;
   int grid = (int)std::max<int64_t>(1, std::min(want, cap));
   blas_kernel<K, OP, STRAT><<<grid, 256, 0, st>>>(a, b, out, n, args);
   WM_LAUNCH_CHECK("blas_kernel launch");
