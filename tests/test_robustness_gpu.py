@@ -138,6 +138,8 @@ def test_plan_creation_leaves_other_streams_running(cuda):
     # context on a kernel's first load), so it is created before the side work
     prm = find_ntt_params(128, 1 << 10)
     field = dev.Field(128, prm.p)
+    import gc
+    gc.collect()
     side = torch.cuda.Stream()
     big = torch.empty(1 << 28, dtype=torch.int32, device="cuda")
     torch.cuda.synchronize()
@@ -145,9 +147,18 @@ def test_plan_creation_leaves_other_streams_running(cuda):
         torch.cuda._sleep(int(2e9))  # ~1 s of GPU clock cycles
         big.add_(1)
     # keep the plan alive past the check: destroying it frees device memory
-    # (cudaFree synchronises the device by definition)
-    plan = dev.NttPlan(field, prm)
-    busy = not side.query()
+    # (cudaFree synchronises the device by definition).  Earlier tests' plans
+    # and fields still waiting for the garbage collector would do the same if
+    # a collection ran inside the measured call, so collect first and keep
+    # the collector off while measuring.
+    import gc
+    gc.collect()
+    gc.disable()
+    try:
+        plan = dev.NttPlan(field, prm)
+        busy = not side.query()
+    finally:
+        gc.enable()
     torch.cuda.synchronize()
     del plan
     assert busy, "plan creation waited for an unrelated stream"
