@@ -291,6 +291,10 @@ def run_gpu(args, rank, world, local, pg):
 
     pass0_ms = statistics.mean(a.elapsed_time(b) for a, b in fwd_ev)
 
+    # ---- end-to-end through the C ABI with host buffers (reference layout),
+    # before the generic-path plan and its buffers are allocated
+    e2e = run_e2e(args, torch, plan, bufs, pg, world)
+
     # ---- the same step through the generic Barrett/Shoup path (reduction="barrett")
     generic = None
     if want(args, "generic"):
@@ -317,9 +321,6 @@ def run_gpu(args, rank, world, local, pg):
                    "note": "the headline step with WM_FIELD_BARRETT: Shoup butterflies (MODE 0), same inputs, "
                            "same timing protocol"}
         del gplan, gws
-
-    # ---- end-to-end through the C ABI with host buffers (reference layout)
-    e2e = run_e2e(args, torch, plan, bufs, pg, world)
 
     # ---- extras: BLAS sweep (configs[2]), four-step single 2^24 NTT (configs[4]), reference GPU code
     blas = run_blas(args, torch, field, rank, world, pg) if want(args, "blas") else None

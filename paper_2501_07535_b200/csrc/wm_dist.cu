@@ -212,13 +212,24 @@ __global__ void twiddle_2d_kernel(uint32_t *table, int64_t n, int64_t row0, int6
 // 2^24 / P pairs (1 GiB / P).
 enum { kDistBarrett = 0, kDistMont = 1, kDistPm = 3 };
 
+// Full products of the special-form twiddle multiply: Karatsuba for 8..16
+// limbs as in the NTT passes (pm_ntt_strat), schoolbook elsewhere.
+template <int K>
+__host__ __device__ constexpr int fx_pm_strat() {
+#ifdef WM_FX_STRAT
+  return WM_FX_STRAT;
+#else
+  return (K >= 8 && K <= 16) ? kKaratsuba : kSchoolbook;
+#endif
+}
+
 template <int K, int MODE>
 WM_DEV void dist_twiddle_mul(uint32_t (&res)[K], const uint32_t (&v)[K], const uint32_t (&lo)[K],
                              const uint32_t (&hi)[K], const FieldConst<K> &F) {
   uint32_t w[K];
   if constexpr (MODE == kDistPm) {
-    mul_pm_lazy<K>(w, hi, lo, F.pm_c, F.pm_sh);   // w < 2q
-    mul_pm_lazy<K>(res, w, v, F.pm_c, F.pm_sh);   // < 2^m + 2^68
+    mul_pm_lazy<K, fx_pm_strat<K>()>(w, hi, lo, F.pm_c, F.pm_sh);   // w < 2q
+    mul_pm_lazy<K, fx_pm_strat<K>()>(res, w, v, F.pm_c, F.pm_sh);   // < 2^m + 2^68
     cond_sub<K>(res, F.q);
   } else if constexpr (MODE == kDistMont) {
     mont_mul<K>(w, hi, lo, F.q, F.qinv);  // (hi lo) R

@@ -15,6 +15,7 @@
 // kComp compute streams and the kernels of consecutive chunks run
 // concurrently; the copies, not the kernels, then bound the pipeline.
 #include <algorithm>
+#include <cstdlib>
 #include <functional>
 #include <vector>
 
@@ -111,6 +112,11 @@ static int run_pipeline(HostPipe &hp, const std::vector<int64_t> &sizes, int nin
   int rc = hp.ensure((int64_t)slot);
   if (rc) return rc;
   cudaStream_t h2d = hp.hs[0], d2h = hp.hs[1];
+  static const int ahead = [] {
+    const char *e = getenv("WM_HOST_AHEAD");  // A/B knob (profiles/r02_e2e_ahead.txt)
+    const int v = e ? atoi(e) : HostPipe::kSlots;
+    return std::min(std::max(v, 1), HostPipe::kSlots);
+  }();
   WM_CUDA_TRY(cudaEventRecord(hp.ev_entry, user));
   for (int i = 0; i < HostPipe::kStreams; ++i) WM_CUDA_TRY(cudaStreamWaitEvent(hp.hs[i], hp.ev_entry, 0));
   int64_t u0 = 0;
@@ -120,7 +126,9 @@ static int run_pipeline(HostPipe &hp, const std::vector<int64_t> &sizes, int nin
     const int64_t nt = sizes[c];
     char *base = static_cast<char *>(hp.slot_mem[s]);
     void *d_in[4];
-    if (c >= (size_t)HostPipe::kSlots) WM_CUDA_TRY(cudaStreamWaitEvent(h2d, hp.ev_out[s], 0));
+    // H2D may run `ahead` chunks in front of the D2H stream (slot reuse needs
+    // ahead <= kSlots); a shorter lead keeps both copy directions busy together
+    if (c >= (size_t)ahead) WM_CUDA_TRY(cudaStreamWaitEvent(h2d, hp.ev_out[(c - ahead) % HostPipe::kSlots], 0));
     for (int k = 0; k < nin; ++k) {
       d_in[k] = base + k * in_sz;
       WM_CUDA_TRY(cudaMemcpyAsync(d_in[k], static_cast<const char *>(host_in[k]) + in_unit * u0, in_unit * nt,

@@ -488,6 +488,15 @@ WM_DEV void twimg_wait(uint64_t *mbar) {
   }
 }
 
+// Plan-time zero fill of the twiddle images' padding (a kernel of our own:
+// cudaMemsetAsync's kernel loads lazily on first use, and a module load
+// synchronises the context, i.e. waits for every stream of the device).
+template <int K>
+__global__ void zero_words_kernel(uint32_t *p, int64_t words) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = 0u;
+}
+
 // Plan-time builder of a pass's twiddle image (same layout the pass reads).
 template <int K>
 __global__ void twiddle_image_kernel(const uint32_t *table, int64_t stride, int logL, uint32_t *img) {
@@ -891,7 +900,9 @@ static int create_tables_on(wm_ntt_plan *pl, const Big &root, const Big &root_in
   }
   pl->tw_img_words_dir = words;
   WM_CUDA_TRY(cudaMallocAsync(reinterpret_cast<void **>(&pl->tw_img), 2 * words * sizeof(uint32_t), st));
-  WM_CUDA_TRY(cudaMemsetAsync(pl->tw_img, 0, 2 * words * sizeof(uint32_t), st));
+  zero_words_kernel<K><<<(int)std::min<int64_t>((2 * words + 255) / 256, 1024), 256, 0, st>>>(pl->tw_img,
+                                                                                             2 * (int64_t)words);
+  WM_LAUNCH_CHECK("zero_words launch");
   for (int dir = 0; dir < 2; ++dir) {
     const uint32_t *table = dir ? pl->tw_inv : pl->tw_fwd;
     for (size_t pi = 0; pi < pl->passes.size(); ++pi) {
@@ -948,6 +959,7 @@ int ntt_preload(int mode) {
   cudaFuncAttributes a;
   auto touch = [&](const void *fn) { (void)cudaFuncGetAttributes(&a, fn); };
   touch((const void *)twiddle_image_kernel<K>);
+  touch((const void *)zero_words_kernel<K>);
   if (mode == 1 || mode == 2) {
     if constexpr (mont_ntt_built<K>()) {
       touch((const void *)twiddle_gen_kernel<K, true>);

@@ -47,7 +47,11 @@ def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def split_lengths(n: int) -> tuple[int, int]:
-    """n = N1 * N2 with N1 >= N2, both powers of two (N1 = 2^ceil(log n / 2))."""
+    """n = N1 * N2 with N1 >= N2, both powers of two (N1 = 2^ceil(log n / 2)).
+    The balanced split: at 256-bit 2^24 every split between 2^12 x 2^12 and
+    2^16 x 2^8 runs within 2 % of it at one rank (the row passes are
+    integer-bound, so their number matters little; a 2^11-point single pass is
+    7 % slower), profiles/r02_ab_four_step_split.txt."""
     if n < 4 or n & (n - 1):
         raise ValueError("four-step needs a power-of-two length >= 4")
     logn = n.bit_length() - 1
@@ -285,9 +289,11 @@ class FourStepNtt:
     """One length-n NTT across the ranks of a communicator (see module doc)."""
 
     def __init__(self, bits: int, params: NttParams, rank: int, world: int, backend=None, comm=None,
-                 strategy: str = "schoolbook"):
+                 strategy: str = "schoolbook", split: tuple[int, int] | None = None):
         self.params = params
-        self.layout = FourStepLayout(params.n, *split_lengths(params.n), world)
+        if split is None:
+            split = split_lengths(params.n)
+        self.layout = FourStepLayout(params.n, *split, world)
         self.rank, self.world = rank, world
         self.backend = (backend if backend is not None
                         else DeviceBackend(bits, params, self.layout, rank, strategy))

@@ -222,3 +222,32 @@ def test_widemul_full_products(cuda):
             xs = [rnd.getrandbits(bits) for _ in range(500)] + [(1 << bits) - 1, 0, 1]
             ys = [rnd.getrandbits(bits) for _ in range(500)] + [(1 << bits) - 1, (1 << bits) - 1, 1]
             assert K.run_vector(wm, xs, ys) == [a * b for a, b in zip(xs, ys)], (bits, strat)
+
+
+@pytest.mark.parametrize("bits", [32, 64, 128])
+@pytest.mark.parametrize("offset", [0, 1, 3])
+def test_small_elements_packed_and_unaligned(cuda, bits, offset):
+    """1-, 2- and 4-limb elements take packed 256-bit accesses (8/K elements
+    per thread) when the three bases are 32-byte aligned, one element per
+    thread otherwise; both paths and the ragged n % (8/K) tail must agree with
+    Python integers.  Views at an element offset make the bases unaligned."""
+    torch = cuda
+    dev = _dev()
+    rnd = random.Random(bits * 10 + offset)
+    q = (1 << (bits - 4)) - 59 if bits > 32 else 4294967291 >> 4
+    f = dev.Field(bits, q)
+    n = 4099  # odd: every packing leaves a tail
+    xs = [rnd.randrange(q) for _ in range(n + offset)]
+    ys = [rnd.randrange(q) for _ in range(n + offset)]
+    x = dev.to_device(dev.ints_to_limbs(xs, f.limbs))[offset:]
+    y = dev.to_device(dev.ints_to_limbs(ys, f.limbs))[offset:]
+    outbuf = torch.empty((n + offset, f.limbs), dtype=torch.int32, device="cuda")
+    out = outbuf[offset:]
+    a, b = xs[offset:], ys[offset:]
+    s = rnd.randrange(q)
+    for kind, want in (("vadd", [(u + v) % q for u, v in zip(a, b)]),
+                       ("vsub", [(u - v) % q for u, v in zip(a, b)]),
+                       ("vmul", [u * v % q for u, v in zip(a, b)]),
+                       ("axpy", [(s * u + v) % q for u, v in zip(a, b)])):
+        r = f.axpy(s, x, y, out=out) if kind == "axpy" else getattr(f, kind)(x, y, out=out)
+        assert dev.limbs_to_ints(dev.to_host(r)) == want, (kind, bits, offset)

@@ -142,6 +142,12 @@ def test_plan_creation_leaves_other_streams_running(cuda):
     gc.collect()
     side = torch.cuda.Stream()
     big = torch.empty(1 << 28, dtype=torch.int32, device="cuda")
+    # torch's own kernels load lazily too: the first launch of the side work's
+    # kernels would synchronise the context right here (before plan creation),
+    # so run them once first
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(1000)
+        big.add_(1)
     torch.cuda.synchronize()
     with torch.cuda.stream(side):
         torch.cuda._sleep(int(2e9))  # ~1 s of GPU clock cycles
@@ -154,12 +160,17 @@ def test_plan_creation_leaves_other_streams_running(cuda):
     import gc
     gc.collect()
     gc.disable()
+    import time
     try:
+        busy_before = not side.query()
+        t0 = time.perf_counter()
         plan = dev.NttPlan(field, prm)
+        took = time.perf_counter() - t0
         busy = not side.query()
     finally:
         gc.enable()
     torch.cuda.synchronize()
     del plan
-    assert busy, "plan creation waited for an unrelated stream"
+    assert busy, (f"plan creation waited for an unrelated stream (side busy before: {busy_before}, "
+                  f"creation took {took * 1e3:.1f} ms)")
     side.synchronize()
