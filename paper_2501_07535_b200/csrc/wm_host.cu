@@ -7,8 +7,9 @@
 // Owner-held streams (HostPipe) form a pipeline over chunks with kSlots
 // staging slots in device memory:
 //   h2d stream:      wait slot free -> memcpy the chunk's inputs -> record ev_in
-//   compute streams: wait ev_in -> ref->limbs, kernels, limbs->ref -> ev_comp
-//   d2h stream:      wait ev_comp -> memcpy to host_out -> record ev_out (slot free)
+//   compute streams: wait ev_in -> ref->limbs, kernels, limbs->ref,
+//                    memcpy to host_out -> record ev_out (slot free)
+// (WM_HOST_POST=0: the D2H copies on a dedicated stream after ev_comp).
 // PCIe is full duplex, so H2D and D2H of different chunks run at once.  A
 // small chunk's kernels fill only part of the GPU (a 2^16-point, 256-bit
 // chunk of 2 transforms is 64 CTAs per pass), so chunks round-robin over
@@ -112,11 +113,16 @@ static int run_pipeline(HostPipe &hp, const std::vector<int64_t> &sizes, int nin
   int rc = hp.ensure((int64_t)slot);
   if (rc) return rc;
   cudaStream_t h2d = hp.hs[0], d2h = hp.hs[1];
-  static const int ahead = [] {
-    const char *e = getenv("WM_HOST_AHEAD");  // A/B knob (profiles/r02_e2e_ahead.txt)
-    const int v = e ? atoi(e) : HostPipe::kSlots;
-    return std::min(std::max(v, 1), HostPipe::kSlots);
-  }();
+  // A/B knobs, read per call so one process can interleave settings
+  const char *e_ahead = getenv("WM_HOST_AHEAD");
+  const int ahead = std::min(std::max(e_ahead ? atoi(e_ahead) : HostPipe::kSlots, 1), HostPipe::kSlots);
+  // Each chunk's D2H is issued on its compute stream right after its kernels
+  // (one cross-stream hop per chunk instead of two): 256-bit 2^16 x 64
+  // forward+inverse 3.24 -> 3.06 ms per call against a 2.68 ms copy floor
+  // (profiles/r02_e2e_ab_post.txt).  WM_HOST_POST=0 restores the dedicated
+  // D2H stream (A/B).
+  const char *e_post = getenv("WM_HOST_POST");
+  const bool post = !e_post || atoi(e_post) != 0;
   WM_CUDA_TRY(cudaEventRecord(hp.ev_entry, user));
   for (int i = 0; i < HostPipe::kStreams; ++i) WM_CUDA_TRY(cudaStreamWaitEvent(hp.hs[i], hp.ev_entry, 0));
   int64_t u0 = 0;
@@ -139,12 +145,23 @@ static int run_pipeline(HostPipe &hp, const std::vector<int64_t> &sizes, int nin
     void *d_out = nullptr;
     rc = fn(nt, d_in, base + nin * in_sz, comp, &d_out);
     if (rc) return rc;
-    WM_CUDA_TRY(cudaEventRecord(hp.ev_comp[s], comp));
-    WM_CUDA_TRY(cudaStreamWaitEvent(d2h, hp.ev_comp[s], 0));
-    WM_CUDA_TRY(cudaMemcpyAsync(static_cast<char *>(host_out) + out_unit * u0, d_out, out_unit * nt,
-                                cudaMemcpyDeviceToHost, d2h));
-    WM_CUDA_TRY(cudaEventRecord(hp.ev_out[s], d2h));
+    if (post) {  // the chunk's D2H follows its kernels on the same stream (one hop fewer)
+      WM_CUDA_TRY(cudaMemcpyAsync(static_cast<char *>(host_out) + out_unit * u0, d_out, out_unit * nt,
+                                  cudaMemcpyDeviceToHost, comp));
+      WM_CUDA_TRY(cudaEventRecord(hp.ev_out[s], comp));
+    } else {
+      WM_CUDA_TRY(cudaEventRecord(hp.ev_comp[s], comp));
+      WM_CUDA_TRY(cudaStreamWaitEvent(d2h, hp.ev_comp[s], 0));
+      WM_CUDA_TRY(cudaMemcpyAsync(static_cast<char *>(host_out) + out_unit * u0, d_out, out_unit * nt,
+                                  cudaMemcpyDeviceToHost, d2h));
+      WM_CUDA_TRY(cudaEventRecord(hp.ev_out[s], d2h));
+    }
     u0 += nt;
+  }
+  if (post) {  // join: the last chunk of every compute stream covers its earlier ones
+    const size_t nc = sizes.size();
+    for (size_t c = nc > (size_t)HostPipe::kComp ? nc - HostPipe::kComp : 0; c < nc; ++c)
+      WM_CUDA_TRY(cudaStreamWaitEvent(d2h, hp.ev_out[c % HostPipe::kSlots], 0));
   }
   WM_CUDA_TRY(cudaEventRecord(hp.ev_done, d2h));
   WM_CUDA_TRY(cudaStreamWaitEvent(user, hp.ev_done, 0));
@@ -171,8 +188,10 @@ extern "C" int wm_ntt_host(const wm_ntt_plan *pc, int mode, int word_bits, int r
   const int64_t n = p->n;
   const int K = p->K;
   // auto chunks: ~8 MiB of limbs (PCIe runs at ~90 GB/s both ways from 4 MiB
-  // chunks up, profiles/r01_pcie_chunks.txt), ramping from one transform
-  const std::vector<int64_t> sizes = chunk_schedule(batch, chunk, (int64_t)(8 << 20) / (n * K * 4), 1);
+  // chunks up, profiles/r01_pcie_chunks.txt); no ramp (with the D2H on the
+  // compute streams the ramped schedule was 1.5 % slower, profiles/r02_e2e_post.txt)
+  const int64_t target = std::max<int64_t>(1, (int64_t)(8 << 20) / (n * K * 4));
+  const std::vector<int64_t> sizes = chunk_schedule(batch, chunk, target, target);
   int64_t max_chunk = 0;
   for (int64_t c : sizes) max_chunk = std::max(max_chunk, c);
   const size_t ref_unit = (size_t)n * ref_words * (word_bits / 8);

@@ -34,7 +34,9 @@ def copies():
 res["floor"] = round(t(copies), 3)
 print(json.dumps(res))
 '''
-for ahead in (1, 2, 3, 4, 8):
-    env = dict(os.environ, WM_HOST_AHEAD=str(ahead))
+settings = [(a, p) for p in (0, 1) for a in (2, 3, 4, 8)] if len(sys.argv) < 2 else \
+    [tuple(int(v) for v in x.split(",")) for x in sys.argv[1:]]
+for ahead, post in settings:
+    env = dict(os.environ, WM_HOST_AHEAD=str(ahead), WM_HOST_POST=str(post))
     out = subprocess.run([sys.executable, "-c", CHILD % str(ROOT)], env=env, capture_output=True, text=True)
-    print("ahead", ahead, out.stdout.strip() or out.stderr[-1500:], flush=True)
+    print("ahead", ahead, "post", post, out.stdout.strip() or out.stderr[-1500:], flush=True)

@@ -2,6 +2,7 @@
 
     python tools/workload.py ntt   [--bits 256 --logn 16 --batch 64 --reps 2]
     python tools/workload.py vmul  [--bits 256 --logn 24 --reps 2]
+    python tools/workload.py four_step [--bits 256 --logn 24 --reps 2]   (one rank, local exchange)
 """
 import argparse
 import sys
@@ -12,7 +13,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("what", choices=["ntt", "vmul", "vadd", "axpy"])
+    ap.add_argument("what", choices=["ntt", "vmul", "vadd", "axpy", "four_step"])
     ap.add_argument("--bits", type=int, default=256)
     ap.add_argument("--logn", type=int, default=None)
     ap.add_argument("--batch", type=int, default=64)
@@ -42,6 +43,19 @@ def main():
         for _ in range(a.reps):
             plan.forward(x, out=y, workspace=ws)
             plan.inverse(y, out=x, workspace=ws)
+    elif a.what == "four_step":
+        from paper_2501_07535_b200 import dist as D
+        logn = a.logn or 24
+
+        class SelfComm:
+            def all_to_all(self, out, inp):
+                out.copy_(inp)
+
+        eng = D.FourStepNtt(a.bits, find_ntt_params(a.bits, 1 << logn), 0, 1, comm=SelfComm())
+        L = eng.layout
+        x = rand(L.n1 * L.n2, 1).view(L.n1, L.n2, Kl)
+        for _ in range(a.reps):
+            eng.forward(x)
     else:
         logn = a.logn or 24
         kara_from = 12 if a.reduction == "auto" else 8  # the bench's choice (bench.py run_blas)
