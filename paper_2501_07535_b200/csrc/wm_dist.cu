@@ -247,6 +247,20 @@ struct FxArgs {
   int layout;    // scatter layout: 0 [src][c_local][rows], 1 [c_local][P * rows] (rows of the next phase)
 };
 
+// Shared-memory tile of the twiddle/transpose kernel: elements at an odd
+// word pitch (conflict-free stores of a warp's 32 consecutive columns) in
+// rows padded so that consecutive rows start K banks apart (conflict-free
+// reads of the transposed K-word runs); ncu showed 43 M bank conflicts in
+// 51 M wavefronts with the K-word pitch (profiles/r02b_ncu_summary.jsonl).
+template <int K>
+__host__ __device__ constexpr int fx_elem_pitch() {
+  return (K % 2 == 0) ? K + 1 : K;
+}
+template <int K>
+__host__ __device__ constexpr int fx_row_pitch() {
+  return TT * fx_elem_pitch<K>() + (((K - TT * fx_elem_pitch<K>()) % 32) + 32) % 32;
+}
+
 // out[c][r] = in[r][c] * root^((row0 + r) c mod n), canonical, twiddles from
 // the factor tables.  With a ScatterDst, output row c goes to rank
 // d = c / cpr: layout 0 at [src][c mod cpr][r] (the block layout of an
@@ -258,9 +272,9 @@ __global__ void __launch_bounds__(256) scale_transpose_fx_kernel(const uint32_t 
                                                                  int64_t cols, const __grid_constant__ FieldConst<K> F,
                                                                  const __grid_constant__ ScatterDst D,
                                                                  const FxArgs A) {
-  extern __shared__ uint32_t tile[];  // TT * (TT*K + 1)
+  extern __shared__ uint32_t tile[];  // TT * fx_row_pitch<K>() words
   const int64_t r0 = (int64_t)blockIdx.y * TT, c0 = (int64_t)blockIdx.x * TT;
-  const int stride = TT * K + 1;
+  constexpr int EP = fx_elem_pitch<K>(), stride = fx_row_pitch<K>();
   const uint64_t nmask = (uint64_t)A.n - 1, lmask = ((uint64_t)1 << A.logB) - 1;
   for (int idx = threadIdx.x; idx < TT * TT; idx += blockDim.x) {
     const int rr = idx / TT, cc = idx - rr * TT;
@@ -273,7 +287,7 @@ __global__ void __launch_bounds__(256) scale_transpose_fx_kernel(const uint32_t 
       ldg_elem<K>(hi, hi_t + (e >> A.logB) * K);
       dist_twiddle_mul<K, MODE>(res, v, lo, hi, F);
 #pragma unroll
-      for (int j = 0; j < K; ++j) tile[rr * stride + cc * K + j] = res[j];
+      for (int j = 0; j < K; ++j) tile[rr * stride + cc * EP + j] = res[j];
     }
   }
   __syncthreads();
@@ -291,7 +305,7 @@ __global__ void __launch_bounds__(256) scale_transpose_fx_kernel(const uint32_t 
       } else {
         row_base = out + c * rows * K;
       }
-      row_base[r0 * K + w] = tile[rr * stride + cc * K + ww];
+      row_base[r0 * K + w] = tile[rr * stride + cc * EP + ww];
     }
   }
 }
@@ -321,7 +335,7 @@ __global__ void twiddle_factor_kernel(uint32_t *table, int64_t count, int64_t st
 template <int K, int MODE>
 static int launch_fx_t(const wm_field *f, const uint32_t *in, const uint32_t *lo, const uint32_t *hi, uint32_t *out,
                        int64_t rows, int64_t cols, cudaStream_t st, const ScatterDst &D, const FxArgs &A) {
-  const size_t smem = (size_t)TT * (TT * K + 1) * 4;
+  const size_t smem = (size_t)TT * fx_row_pitch<K>() * 4;
   static std::atomic<uint64_t> attr{0};
   if (first_on_device(attr)) {
     WM_CUDA_TRY(cudaFuncSetAttribute(scale_transpose_fx_kernel<K, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
