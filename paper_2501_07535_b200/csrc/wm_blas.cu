@@ -165,8 +165,11 @@ constexpr int kMontField = 2;
 constexpr int kPmField = 3;
 constexpr int kPmKara = 4;
 
-#ifndef WM_BLAS_MINB_WIDE  // resident CTAs requested for K >= 16 (register cap)
-#define WM_BLAS_MINB_WIDE 1
+#ifndef WM_BLAS_MINB_WIDE  // resident CTAs requested for 16 <= K <= 24 (register cap 128):
+#define WM_BLAS_MINB_WIDE 2   // 768-bit Karatsuba vmul/axpy 2.84 -> 3.30 / 2.50 -> 3.40 TB/s
+#endif                        // (228 -> 128 registers, 24 B spilled; profiles/r02_ab_blas_wide_minb.txt)
+#ifndef WM_BLAS_MINB_HUGE  // K = 32: 2 CTAs/SM would spill 0.3-0.8 KB per thread
+#define WM_BLAS_MINB_HUGE 1
 #endif
 #ifndef WM_BLAS_MINB_MID  // 9 <= K <= 15: 3 CTAs/SM (<= 85 registers)
 #define WM_BLAS_MINB_MID 3
@@ -236,7 +239,7 @@ WM_DEV void blas_elem(uint32_t (&r)[K], const uint32_t (&x)[K], const uint32_t (
 #endif
 
 template <int K, int OP, int STRAT>
-__global__ void __launch_bounds__(256, (K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? WM_BLAS_MINB_MID : K <= 4 && OP <= OP_VSUB ? WM_BLAS_MINB_SMALL : 1)) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
+__global__ void __launch_bounds__(256, (K > 24 ? WM_BLAS_MINB_HUGE : K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? WM_BLAS_MINB_MID : K <= 4 && OP <= OP_VSUB ? WM_BLAS_MINB_SMALL : 1)) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
                                                    int64_t n, const __grid_constant__ BlasArgs<K> args) {
   constexpr int E = K <= 4 ? WM_BLAS_EPT_SMALL : 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -248,6 +251,9 @@ __global__ void __launch_bounds__(256, (K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? W
   if constexpr (PK > 1 && (WM_BLAS_PACK_OPS >> OP) & 1) {
     if ((((uintptr_t)a | (uintptr_t)b | (uintptr_t)out) & 31u) == 0) {
       const int64_t groups = n / PK;
+      // no unrolling: the trip count is ~1 (one thread per group); an
+      // unrolled grid-stride loop costs a 64-bit division per thread up front
+#pragma unroll 1
       for (int64_t gi = i; gi < groups; gi += stride) {
         uint32_t xa[8], ya[8], ra[8];
         ld8_stream(xa, a + gi * 8);
@@ -283,6 +289,7 @@ __global__ void __launch_bounds__(256, (K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? W
       for (int e = 0; e < E; ++e) store_elem<K>(out, i + e * stride, r[e]);
     }
   }
+#pragma unroll 1
   for (; i < n; i += stride) {
     uint32_t x[K], y[K], r[K];
     if constexpr (K <= 4 && (OP == OP_VADD || OP == OP_VSUB) && WM_BLAS_SMALL_IO == 1) {

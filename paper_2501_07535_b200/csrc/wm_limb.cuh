@@ -329,7 +329,10 @@ WM_DEV void mul_full_s(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint3
 template <int K, int ST>
 WM_DEV void mul_full_kara(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
   constexpr int H = K / 2;
-  constexpr int SUB = (H >= 8 && (H % 2) == 0) ? kKaratsuba : kSchoolbook;
+#ifndef WM_KARA_REC_MIN  // recurse while the half has at least this many limbs
+#define WM_KARA_REC_MIN 8
+#endif
+  constexpr int SUB = (H >= WM_KARA_REC_MIN && (H % 2) == 0) ? kKaratsuba : kSchoolbook;
   uint32_t a0[H], a1[H], b0[H], b1[H];
 #pragma unroll
   for (int j = 0; j < H; ++j) {
