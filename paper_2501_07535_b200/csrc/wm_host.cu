@@ -191,7 +191,9 @@ extern "C" int wm_ntt_host(const wm_ntt_plan *pc, int mode, int word_bits, int r
   // chunks up, profiles/r01_pcie_chunks.txt); no ramp (with the D2H on the
   // compute streams the ramped schedule was 1.5 % slower, profiles/r02_e2e_post.txt)
   const int64_t target = std::max<int64_t>(1, (int64_t)(8 << 20) / (n * K * 4));
-  const std::vector<int64_t> sizes = chunk_schedule(batch, chunk, target, target);
+  const char *e_ramp = getenv("WM_HOST_RAMP");  // A/B knob: ramp the chunk sizes from this many transforms
+  const int64_t ramp_from = e_ramp && atoi(e_ramp) > 0 ? atoi(e_ramp) : target;
+  const std::vector<int64_t> sizes = chunk_schedule(batch, chunk, target, ramp_from);
   int64_t max_chunk = 0;
   for (int64_t c : sizes) max_chunk = std::max(max_chunk, c);
   const size_t ref_unit = (size_t)n * ref_words * (word_bits / 8);

@@ -25,12 +25,16 @@ def copies():
     with torch.cuda.stream(s_in): dev_buf.copy_(h, non_blocking=True)
     with torch.cuda.stream(s_out): h.copy_(dev_src, non_blocking=True)
     st.wait_stream(s_in); st.wait_stream(s_out)
-rows = {k: [] for k in ("floor", "post0_auto", "post1_auto", "post0_c4", "post1_c4", "post1_c2", "post1_c8")}
+settings = [("post0", {"WM_HOST_POST": "0"}), ("post1", {"WM_HOST_POST": "1"}),
+            ("post1_ramp1", {"WM_HOST_POST": "1", "WM_HOST_RAMP": "1"}),
+            ("post1_ramp2", {"WM_HOST_POST": "1", "WM_HOST_RAMP": "2"})]
+rows = {k: [] for k in ["floor"] + [name for name, _ in settings]}
 for rep in range(6):
     rows["floor"].append(t(copies))
-    for post in (0, 1):
-        os.environ["WM_HOST_POST"] = str(post)
-        for chunk, tag in ((0, "auto"), (4, "c4")) + (((2, "c2"), (8, "c8")) if post else ()):
-            rows[f"post{post}_{tag}"].append(t(lambda: plan.host_transform(h, h, mode="forward_inverse", word_bits=64,
-                                                                             ref_words=4, chunk=chunk)))
+    for name, env in settings:
+        for k in ("WM_HOST_POST", "WM_HOST_RAMP"):
+            os.environ.pop(k, None)
+        os.environ.update(env)
+        rows[name].append(t(lambda: plan.host_transform(h, h, mode="forward_inverse", word_bits=64, ref_words=4,
+                                                          chunk=0)))
 print(json.dumps({k: {"median_ms": round(statistics.median(v), 3), "all": [round(x, 3) for x in v]} for k, v in rows.items()}))
