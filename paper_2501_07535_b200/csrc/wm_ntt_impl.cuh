@@ -433,6 +433,10 @@ __device__ __forceinline__ void dft_smem(uint32_t *data, const uint32_t *tww, co
   }
 }
 
+#ifndef WM_ROW_EPI_GFAST
+#define WM_ROW_EPI_GFAST 1  // 8.536 -> 8.506 us/transform (profiles/r02_ab_row_epilogue.txt)
+#endif
+
 // Global loads kept in flight per thread while a pass stages its tile.
 template <int K>
 constexpr int kLoadU = K <= 8 ? 4 : (K <= 16 ? 2 : 1);
@@ -638,7 +642,15 @@ __global__ void WM_NTT_BOUNDS(K, MODE) ntt_row_pass(const uint32_t *in, uint32_t
   twimg_wait(mbar);
   dft_smem<K, MODE>(data, tww, twp, logL, G, c);
   for (int idx = threadIdx.x; idx < G * L; idx += blockDim.x) {
+    // WM_ROW_EPI_GFAST: consecutive lanes take consecutive lines (output
+    // elements k*WK + r are adjacent in r), G*32 B contiguous per store group
+    // instead of one 32-B sector per lane; the swizzled tile reads this
+    // order conflict-free (the column pass epilogue's order)
+#if WM_ROW_EPI_GFAST
+    const int g = idx & (G - 1), k = idx >> d.logG;
+#else
     const int g = idx >> logL, k = idx & (L - 1);
+#endif
     const int64_t lam = lam0 + g;
     if (lam < d.total_lines) {
       const int64_t b = lam >> d.log_inner, r = lam & inner_mask;
