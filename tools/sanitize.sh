@@ -7,3 +7,7 @@ done
 echo "== memcheck blas"
 timeout 600 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/workload.py vmul --logn 14 --reps 1 2>&1 | tail -3
 timeout 600 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/workload.py vmul --bits 384 --logn 14 --reps 1 2>&1 | tail -3
+echo "== memcheck/racecheck round-2 paths (packed small-element BLAS, four-step twiddle/transpose tile)"
+timeout 600 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/workload.py vadd --bits 128 --logn 14 --reps 1 2>&1 | tail -3
+timeout 600 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/workload.py four_step --logn 14 --reps 1 2>&1 | tail -3
+timeout 600 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/workload.py four_step --logn 14 --reps 1 2>&1 | tail -3

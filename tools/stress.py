@@ -44,22 +44,29 @@ while time.time() < t_end:
             strat = rnd.choice(["schoolbook", "karatsuba", "montgomery"])
             if strat == "montgomery":
                 q = rnd.randrange(3, 1 << bits) | 1
+            elif bits >= 96 and rnd.random() < 0.4 and max(72, 32 * ((bits + 31) // 32) - 31) < bits - 3:
+                # special form q = 2^m - c, c < 2^32 (the two-fold reduction path;
+                # m within 31 bits of the limb top and below 2^(bits-4))
+                mm = rnd.randrange(max(72, 32 * ((bits + 31) // 32) - 31), bits - 3)
+                q = (1 << mm) - rnd.randrange(1, 1 << 32)
             try:
                 f = dev.Field(bits, q, strat)
             except Exception:
                 continue
             m = rnd.randint(1, 3000)
-            xs = [rnd.randrange(q) for _ in range(m)]
-            ys = [rnd.randrange(q) for _ in range(m)]
+            off = rnd.choice([0, 0, 1, 3])  # element offset: unaligned bases (no packed accesses)
+            xs = [rnd.randrange(q) for _ in range(m + off)]
+            ys = [rnd.randrange(q) for _ in range(m + off)]
             op = rnd.choice(["vadd", "vsub", "vmul", "axpy"])
-            x = dev.to_device(dev.ints_to_limbs(xs, f.limbs))
-            y = dev.to_device(dev.ints_to_limbs(ys, f.limbs))
+            x = dev.to_device(dev.ints_to_limbs(xs, f.limbs))[off:]
+            y = dev.to_device(dev.ints_to_limbs(ys, f.limbs))[off:]
+            xs, ys = xs[off:], ys[off:]
             s = rnd.randrange(q)
             out = dev.limbs_to_ints(dev.to_host(f.axpy(s, x, y) if op == "axpy" else getattr(f, op)(x, y)))
             want = {"vadd": [(a + b) % q for a, b in zip(xs, ys)], "vsub": [(a - b) % q for a, b in zip(xs, ys)],
                     "vmul": [a * b % q for a, b in zip(xs, ys)], "axpy": [(s * a + b) % q for a, b in zip(xs, ys)]}[op]
             ok = out == want
-            tag = (kind, op, bits, strat, hex(q)[:12], m)
+            tag = (kind, op, bits, strat, f.reduction, hex(q)[:12], m, off)
         else:
             if bits < 32:
                 continue
