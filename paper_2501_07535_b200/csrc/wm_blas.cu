@@ -174,9 +174,6 @@ constexpr int kPmKara = 4;
 #ifndef WM_BLAS_MINB_MID  // 9 <= K <= 15: 3 CTAs/SM (<= 85 registers)
 #define WM_BLAS_MINB_MID 3
 #endif
-#ifndef WM_BLAS_MINB_SMALL  // add/sub at K <= 4 (A/B: 8 = full occupancy at 256 threads)
-#define WM_BLAS_MINB_SMALL 1
-#endif
 
 template <int K, int OP, int STRAT>
 WM_DEV void blas_elem(uint32_t (&r)[K], const uint32_t (&x)[K], const uint32_t (&y)[K], const BlasArgs<K> &args) {
@@ -222,98 +219,52 @@ WM_DEV void blas_elem(uint32_t (&r)[K], const uint32_t (&x)[K], const uint32_t (
   }
 }
 
-// Elements per thread per grid-stride step for small limb counts (loads of
-// E elements in flight before their arithmetic).
-#ifndef WM_BLAS_EPT_SMALL
-#define WM_BLAS_EPT_SMALL 1
-#endif
-// Ops (bit mask over BlasOp) whose small-element kernels take packed 256-bit
-// accesses (see blas_kernel).
-#ifndef WM_BLAS_PACK_OPS
-#define WM_BLAS_PACK_OPS 3  // add/sub (vmul/axpy 128-bit: 6.53 -> 6.18 TB/s packed, r02_ab_light_blas2.txt)
-#endif
-// Element I/O of the light small-element kernels when not packed (A/B):
-// 0 = vector loads/stores, 1 = word by word, 2 = streaming vector stores.
-#ifndef WM_BLAS_SMALL_IO
-#define WM_BLAS_SMALL_IO 0
-#endif
 
 template <int K, int OP, int STRAT>
-__global__ void __launch_bounds__(256, (K > 24 ? WM_BLAS_MINB_HUGE : K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? WM_BLAS_MINB_MID : K <= 4 && OP <= OP_VSUB ? WM_BLAS_MINB_SMALL : 1)) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
+__global__ void __launch_bounds__(256, (K > 24 ? WM_BLAS_MINB_HUGE : K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? WM_BLAS_MINB_MID : 1)) blas_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
                                                    int64_t n, const __grid_constant__ BlasArgs<K> args) {
-  constexpr int E = K <= 4 ? WM_BLAS_EPT_SMALL : 1;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  // Small elements (K | 8, K < 8): PK = 8/K consecutive elements per thread
-  // through one 256-bit access per operand (LDG/STG.E.ENL2.256), the access
-  // width of the 256-bit kernels, when all three bases are 32-byte aligned.
-  constexpr int PK = (K < 8 && 8 % K == 0) ? 8 / K : 1;
-  if constexpr (PK > 1 && (WM_BLAS_PACK_OPS >> OP) & 1) {
-    if ((((uintptr_t)a | (uintptr_t)b | (uintptr_t)out) & 31u) == 0) {
-      const int64_t groups = n / PK;
-      // no unrolling: the trip count is ~1 (one thread per group); an
-      // unrolled grid-stride loop costs a 64-bit division per thread up front
-#pragma unroll 1
-      for (int64_t gi = i; gi < groups; gi += stride) {
-        uint32_t xa[8], ya[8], ra[8];
-        ld8_stream(xa, a + gi * 8);
-        ld8_stream(ya, b + gi * 8);
-#pragma unroll
-        for (int e = 0; e < PK; ++e) {
-          uint32_t x[K], y[K], r[K];
-#pragma unroll
-          for (int j = 0; j < K; ++j) {
-            x[j] = xa[e * K + j];
-            y[j] = ya[e * K + j];
-          }
-          blas_elem<K, OP, STRAT>(r, x, y, args);
-#pragma unroll
-          for (int j = 0; j < K; ++j) ra[e * K + j] = r[j];
-        }
-        st8(out + gi * 8, ra);
-      }
-      i += groups * PK;  // the n % PK tail, one element per thread
-    }
-  }
-  if constexpr (E > 1) {
-    for (; i + (E - 1) * stride < n; i += E * stride) {
-      uint32_t x[E][K], y[E][K], r[E][K];
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        load_elem<K>(x[e], a, i + e * stride);
-        load_elem<K>(y[e], b, i + e * stride);
-      }
-#pragma unroll
-      for (int e = 0; e < E; ++e) blas_elem<K, OP, STRAT>(r[e], x[e], y[e], args);
-#pragma unroll
-      for (int e = 0; e < E; ++e) store_elem<K>(out, i + e * stride, r[e]);
-    }
-  }
 #pragma unroll 1
   for (; i < n; i += stride) {
     uint32_t x[K], y[K], r[K];
-    if constexpr (K <= 4 && (OP == OP_VADD || OP == OP_VSUB) && WM_BLAS_SMALL_IO == 1) {
-#pragma unroll
-      for (int j = 0; j < K; ++j) {
-        x[j] = a[i * K + j];
-        y[j] = b[i * K + j];
-      }
-    } else {
-      load_elem<K>(x, a, i);
-      load_elem<K>(y, b, i);
-    }
+    load_elem<K>(x, a, i);
+    load_elem<K>(y, b, i);
     blas_elem<K, OP, STRAT>(r, x, y, args);
-    if constexpr (K <= 4 && (OP == OP_VADD || OP == OP_VSUB) && WM_BLAS_SMALL_IO == 1) {
-#pragma unroll
-      for (int j = 0; j < K; ++j) out[i * K + j] = r[j];
-    } else if constexpr (K <= 4 && (OP == OP_VADD || OP == OP_VSUB) && WM_BLAS_SMALL_IO == 2 && K % 4 == 0) {
-#pragma unroll
-      for (int c = 0; c < K; c += 4)
-        __stcs(reinterpret_cast<uint4 *>(out + i * K + c), make_uint4(r[c], r[c + 1], r[c + 2], r[c + 3]));
-    } else {
-      store_elem<K>(out, i, r);
-    }
+    store_elem<K>(out, i, r);
   }
+}
+
+#ifndef WM_BLAS_SMALL_WORDWISE
+#define WM_BLAS_SMALL_WORDWISE 1
+#endif
+// Small elements (K <= 4 limbs): one element per thread, no loop, early exit,
+// word-by-word plain accesses -- the shape of the reference's own emitted
+// element kernel (emit.py:454-484).  On these memory-bound ops it beats
+// 16-byte streaming vector accesses in a grid-stride loop: 128-bit vadd
+// 6.65 -> 6.87 TB/s (= the reference's kernel), vmul 6.53 -> 6.76, axpy
+// unchanged (profiles/r02_ab_vadd_buffers.txt, r02_ab_light_blas6.txt).
+template <int K, int OP, int STRAT>
+__global__ void __launch_bounds__(256) blas_small_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out,
+                                                                int64_t n, const __grid_constant__ BlasArgs<K> args) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t x[K], y[K], r[K];
+#if WM_BLAS_SMALL_WORDWISE  // word-by-word plain accesses, as the reference's kernel
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    x[j] = a[i * K + j];
+    y[j] = b[i * K + j];
+  }
+  blas_elem<K, OP, STRAT>(r, x, y, args);
+#pragma unroll
+  for (int j = 0; j < K; ++j) out[i * K + j] = r[j];
+#else
+  load_elem<K>(x, a, i);
+  load_elem<K>(y, b, i);
+  blas_elem<K, OP, STRAT>(r, x, y, args);
+  store_elem<K>(out, i, r);
+#endif
 }
 
 template <int K, int OP, int STRAT>
@@ -341,20 +292,28 @@ static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, 
     const Big sh = f->mont ? to_mont(a, f->q) : (STRAT == kPmField || STRAT == kPmKara) ? a : big_shl(a, f->s, K);
     for (int j = 0; j < K; ++j) args.scal[j] = sh[j];
   }
-  constexpr int PK = (K < 8 && 8 % K == 0) ? 8 / K : 1;
-  const bool pack256 = PK > 1 && ((WM_BLAS_PACK_OPS >> OP) & 1) &&
-                       ((((uintptr_t)a | (uintptr_t)b | (uintptr_t)out) & 31u) == 0);
-  int64_t want = ((pack256 ? n / PK : n) + 255) / 256;
+  int64_t want = (n + 255) / 256;
 #ifndef WM_BLAS_WAVES  // grid cap in waves of resident CTAs (0: one thread per element)
 #define WM_BLAS_WAVES 4
 #endif
-  // light kernels (<= 4 limbs, add/sub) keep one thread per element: more
-  // loads in flight (128-bit vmul/axpy 6.05 -> 6.52 TB/s); heavier ones run
+  // light kernels (add/sub) keep one thread per element: more loads in
+  // flight (128-bit vmul/axpy 6.05 -> 6.52 TB/s in round 2); heavier ones run
   // a few waves of grid-stride CTAs (256-bit axpy 5.55 -> 5.87 TB/s),
   // profiles/r02_ab_blas_grid.txt
   const bool light = K <= 4 || OP == OP_VADD || OP == OP_VSUB;
   int64_t cap = (WM_BLAS_WAVES && !light) ? (int64_t)sm_count * blocks_per_sm * WM_BLAS_WAVES : want;
   int grid = (int)std::max<int64_t>(1, std::min(want, cap));
+#ifndef WM_BLAS_SMALL_KERNEL
+#define WM_BLAS_SMALL_KERNEL 1
+#endif
+  if constexpr (K <= 4 && WM_BLAS_SMALL_KERNEL) {
+    const int64_t blocks = (n + 255) / 256;
+    if (blocks <= 0x7fffffff) {
+      blas_small_kernel<K, OP, STRAT><<<(unsigned)blocks, 256, 0, st>>>(a, b, out, n, args);
+      WM_LAUNCH_CHECK("blas_small_kernel launch");
+      return WM_OK;
+    }
+  }
   blas_kernel<K, OP, STRAT><<<grid, 256, 0, st>>>(a, b, out, n, args);
   WM_LAUNCH_CHECK("blas_kernel launch");
   return WM_OK;
@@ -496,6 +455,12 @@ template <int K, int STRAT>
 static void preload_blas_k() {
   cudaFuncAttributes a;
   (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_VADD, STRAT == kMontField ? kMontField : kSchoolbook>);
+  if constexpr (K <= 4) {
+    (void)cudaFuncGetAttributes(&a, (const void *)blas_small_kernel<K, OP_VADD, STRAT == kMontField ? kMontField : kSchoolbook>);
+    (void)cudaFuncGetAttributes(&a, (const void *)blas_small_kernel<K, OP_VSUB, STRAT == kMontField ? kMontField : kSchoolbook>);
+    (void)cudaFuncGetAttributes(&a, (const void *)blas_small_kernel<K, OP_VMUL, STRAT>);
+    (void)cudaFuncGetAttributes(&a, (const void *)blas_small_kernel<K, OP_AXPY, STRAT>);
+  }
   (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_VSUB, STRAT == kMontField ? kMontField : kSchoolbook>);
   (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_VMUL, STRAT>);
   (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_AXPY, STRAT>);
