@@ -606,6 +606,7 @@ def run_four_step(args, torch, rank, world, pg):
         comm = D.StagedComm()
     else:
         comm = D.TorchComm()
+    torch.cuda.empty_cache()  # the BLAS sweep's multi-GB operands leave the allocator fragmented
     eng = D.FourStepNtt(BITS, prm, rank, world, comm=comm)
     L = eng.layout
     rows = L.n1 // world
@@ -616,6 +617,9 @@ def run_four_step(args, torch, rank, world, pg):
     back = eng.inverse(y)
     torch.cuda.synchronize()
     assert torch.equal(back, x), "four-step roundtrip mismatch"
+    for _ in range(2):  # the forward's buffers cached again after the inverse's shapes
+        eng.forward(x)
+    torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     reps = 5
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
