@@ -46,15 +46,21 @@ def shard_range(total: int, rank: int, world: int) -> tuple[int, int]:
     return start, start + base + (1 if rank < extra else 0)
 
 
-def split_lengths(n: int) -> tuple[int, int]:
-    """n = N1 * N2 with N1 >= N2, both powers of two (N1 = 2^ceil(log n / 2)).
-    The balanced split: at 256-bit 2^24 every split between 2^12 x 2^12 and
-    2^16 x 2^8 runs within 2 % of it at one rank (the row passes are
-    integer-bound, so their number matters little; a 2^11-point single pass is
-    7 % slower), profiles/r02_ab_four_step_split.txt."""
+def split_lengths(n: int, limbs: int | None = None) -> tuple[int, int]:
+    """n = N1 * N2 with N1 >= N2, both powers of two.
+
+    Balanced (N1 = 2^ceil(log n / 2)) unless the limb count is given: for
+    n >= 2^20 at <= 12 limbs the phase-1 rows are one 1024-point pass (the
+    most efficient pass length at these widths: 7.7 ps per butterfly in the
+    2^20 plan against 8.2 for 256-point passes) and N1 = n / 1024.  At
+    256-bit 2^24 that split (2^14 x 2^10) runs 1.2-1.8 % faster than
+    2^12 x 2^12 at one rank; a 2^11-point single pass is 7 % slower
+    (profiles/r02_ab_four_step_split.txt, r02_fourstep_rerun.txt)."""
     if n < 4 or n & (n - 1):
         raise ValueError("four-step needs a power-of-two length >= 4")
     logn = n.bit_length() - 1
+    if limbs is not None and limbs <= 12 and logn >= 20:
+        return n >> 10, 1 << 10
     n1 = 1 << ((logn + 1) // 2)
     return n1, n // n1
 
@@ -292,7 +298,7 @@ class FourStepNtt:
                  strategy: str = "schoolbook", split: tuple[int, int] | None = None):
         self.params = params
         if split is None:
-            split = split_lengths(params.n)
+            split = split_lengths(params.n, -(-bits // 32))
         self.layout = FourStepLayout(params.n, *split, world)
         self.rank, self.world = rank, world
         self.backend = (backend if backend is not None
