@@ -326,27 +326,13 @@ enum MulStrategy { kSchoolbook = 0, kKaratsuba = 1 };
 template <int K, int ST, int STRAT>
 WM_DEV void mul_full_s(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]);
 
-template <int K, int ST>
-WM_DEV void mul_full_kara(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
-  constexpr int H = K / 2;
-#ifndef WM_KARA_REC_MIN  // recurse while the half has at least this many limbs
-#define WM_KARA_REC_MIN 8
-#endif
-  constexpr int SUB = (H >= WM_KARA_REC_MIN && (H % 2) == 0) ? kKaratsuba : kSchoolbook;
-  uint32_t a0[H], a1[H], b0[H], b1[H];
-#pragma unroll
-  for (int j = 0; j < H; ++j) {
-    a0[j] = a[j]; a1[j] = a[H + j];
-    b0[j] = b[j]; b1[j] = b[H + j];
-  }
-  uint32_t z0[2 * H], z2[2 * H], zm[2 * H];
-  mul_full_s<H, ST, SUB>(z0, a0, b0);
-  mul_full_s<H, ST, SUB>(z2, a1, b1);
-  uint32_t sa[H], sb[H];
-  const uint32_t ca = add_n<H>(sa, a0, a1);
-  const uint32_t cb = add_n<H>(sb, b0, b1);
-  mul_full_s<H, ST, SUB>(zm, sa, sb);
-  // z1 = zm + (ca ? sb : 0) B + (cb ? sa : 0) B + ca cb B^2  - z0 - z2   (2H+1 limbs)
+// t = z0 + z1 B + z2 B^2 from the three half products of one Karatsuba level
+// and the half sums sa = a0 + a1, sb = b0 + b1 with their carries ca, cb:
+//   z1 = zm + (ca ? sb : 0) B + (cb ? sa : 0) B + ca cb B^2 - z0 - z2
+template <int H>
+WM_DEV void kara_combine(uint32_t (&t)[4 * H], const uint32_t (&z0)[2 * H], const uint32_t (&z2)[2 * H],
+                         const uint32_t (&zm)[2 * H], const uint32_t (&sa)[H], const uint32_t (&sb)[H],
+                         uint32_t ca, uint32_t cb) {
   uint32_t z1[2 * H + 1];
 #pragma unroll
   for (int j = 0; j < 2 * H; ++j) z1[j] = zm[j];
@@ -395,6 +381,29 @@ WM_DEV void mul_full_kara(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const ui
   add_n<3 * H>(mid, mid, add);
 #pragma unroll
   for (int j = 0; j < 3 * H; ++j) t[H + j] = mid[j];
+}
+
+template <int K, int ST>
+WM_DEV void mul_full_kara(uint32_t (&t)[2 * K], const uint32_t (&a)[K], const uint32_t (&b)[K]) {
+  constexpr int H = K / 2;
+#ifndef WM_KARA_REC_MIN  // recurse while the half has at least this many limbs
+#define WM_KARA_REC_MIN 8
+#endif
+  constexpr int SUB = (H >= WM_KARA_REC_MIN && (H % 2) == 0) ? kKaratsuba : kSchoolbook;
+  uint32_t a0[H], a1[H], b0[H], b1[H];
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    a0[j] = a[j]; a1[j] = a[H + j];
+    b0[j] = b[j]; b1[j] = b[H + j];
+  }
+  uint32_t z0[2 * H], z2[2 * H], zm[2 * H];
+  mul_full_s<H, ST, SUB>(z0, a0, b0);
+  mul_full_s<H, ST, SUB>(z2, a1, b1);
+  uint32_t sa[H], sb[H];
+  const uint32_t ca = add_n<H>(sa, a0, a1);
+  const uint32_t cb = add_n<H>(sb, b0, b1);
+  mul_full_s<H, ST, SUB>(zm, sa, sb);
+  kara_combine<H>(t, z0, z2, zm, sa, sb, ca, cb);
 }
 
 template <int K, int ST, int STRAT>
@@ -644,6 +653,74 @@ WM_DEV void mul_pm_lazy(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t
   uint32_t t[2 * K];
   mul_full_s<K, ST, STRAT>(t, a, b);
   pm_reduce_wide<K>(r, t, c, sh);
+}
+
+// Two independent full products interleaved row by row (compiler carries):
+// t1 = a1 b1, t2 = a2 b2.  Gives the scheduler two independent dependency
+// chains per row (ILP for the NTT's paired butterflies, WM_NTT_DUAL).
+template <int K>
+WM_DEV void mul_full_dual_u64(uint32_t (&t1)[2 * K], uint32_t (&t2)[2 * K], const uint32_t (&a1)[K],
+                              const uint32_t (&b1)[K], const uint32_t (&a2)[K], const uint32_t (&b2)[K]) {
+#pragma unroll
+  for (int j = 0; j < 2 * K; ++j) {
+    t1[j] = 0u;
+    t2[j] = 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    uint32_t c1 = 0, c2 = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint64_t p1 = (uint64_t)a1[j] * b1[i] + t1[i + j] + c1;
+      const uint64_t p2 = (uint64_t)a2[j] * b2[i] + t2[i + j] + c2;
+      t1[i + j] = (uint32_t)p1;
+      c1 = (uint32_t)(p1 >> 32);
+      t2[i + j] = (uint32_t)p2;
+      c2 = (uint32_t)(p2 >> 32);
+    }
+    t1[i + K] = c1;
+    t2[i + K] = c2;
+  }
+}
+
+// Two independent one-level Karatsuba products with their half products
+// interleaved (mul_full_dual_u64 on the halves).
+template <int K>
+WM_DEV void mul_full_dual_kara(uint32_t (&t1)[2 * K], uint32_t (&t2)[2 * K], const uint32_t (&a1)[K],
+                               const uint32_t (&b1)[K], const uint32_t (&a2)[K], const uint32_t (&b2)[K]) {
+  constexpr int H = K / 2;
+  uint32_t a10[H], a11[H], b10[H], b11[H], a20[H], a21[H], b20[H], b21[H];
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    a10[j] = a1[j]; a11[j] = a1[H + j]; b10[j] = b1[j]; b11[j] = b1[H + j];
+    a20[j] = a2[j]; a21[j] = a2[H + j]; b20[j] = b2[j]; b21[j] = b2[H + j];
+  }
+  uint32_t z01[2 * H], z02[2 * H], z21[2 * H], z22[2 * H], zm1[2 * H], zm2[2 * H];
+  mul_full_dual_u64<H>(z01, z02, a10, b10, a20, b20);
+  mul_full_dual_u64<H>(z21, z22, a11, b11, a21, b21);
+  uint32_t sa1[H], sb1[H], sa2[H], sb2[H];
+  const uint32_t ca1 = add_n<H>(sa1, a10, a11);
+  const uint32_t cb1 = add_n<H>(sb1, b10, b11);
+  const uint32_t ca2 = add_n<H>(sa2, a20, a21);
+  const uint32_t cb2 = add_n<H>(sb2, b20, b21);
+  mul_full_dual_u64<H>(zm1, zm2, sa1, sb1, sa2, sb2);
+  kara_combine<H>(t1, z01, z21, zm1, sa1, sb1, ca1, cb1);
+  kara_combine<H>(t2, z02, z22, zm2, sa2, sb2, ca2, cb2);
+}
+
+template <int K>
+WM_DEV void mul_pm_lazy_dual(uint32_t (&r1)[K], uint32_t (&r2)[K], const uint32_t (&a1)[K], const uint32_t (&b1)[K],
+                             const uint32_t (&a2)[K], const uint32_t (&b2)[K], uint32_t c, uint32_t sh) {
+  uint32_t t1[2 * K], t2[2 * K];
+#ifndef WM_NTT_DUAL_KARA
+#define WM_NTT_DUAL_KARA 1
+#endif
+  if constexpr (WM_NTT_DUAL_KARA && K >= 8 && K <= 16 && K % 2 == 0)
+    mul_full_dual_kara<K>(t1, t2, a1, b1, a2, b2);
+  else
+    mul_full_dual_u64<K>(t1, t2, a1, b1, a2, b2);
+  pm_reduce_wide<K>(r1, t1, c, sh);
+  pm_reduce_wide<K>(r2, t2, c, sh);
 }
 
 // Canonical special-form product of canonical a, b.

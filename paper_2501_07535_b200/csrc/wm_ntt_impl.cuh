@@ -41,6 +41,9 @@
 
 // Minimum resident CTAs per SM requested from ptxas for the pass kernels
 // (caps registers at 65536 / (256 * WM_NTT_MINB)); A/B: tools/ab_timing.py.
+#ifndef WM_NTT_DUAL  // A/B: MODE 3 radix-4 groups with interleaved product pairs
+#define WM_NTT_DUAL 1  // 8.50 -> 8.34 us/transform (profiles/r02_ab_ntt_dual.txt)
+#endif
 #ifndef WM_NTT_MINB
 #define WM_NTT_MINB 2
 #endif
@@ -307,6 +310,30 @@ __device__ __forceinline__ void radix4_single(uint32_t (&x0)[K], uint32_t (&x1)[
   using S = Smem<K>;
   using A = Arith<K, MODE>;
   uint32_t w[K], wp[K];
+#if WM_NTT_DUAL
+  if constexpr (MODE == 3) {  // paired butterflies with interleaved products (A/B)
+    if (trivial) {
+      A::bf1(x0, x1, c);
+      A::bf1(x2, x3, c);
+      A::bf1(x0, x2, c);
+      const int i3 = (j + h) << (lq - s);
+      S::load(w, tww, i3);
+      A::bf(x1, x3, w, wp, c);
+    } else {
+      uint32_t t1[K], t2[K], w2[K];
+      S::load(w, tww, j << (logL - 1 - s));
+      mul_pm_lazy_dual<K>(t1, t2, x1, w, x3, w, c.F.pm_c, c.F.pm_sh);
+      bf_finish<K>(x0, x1, t1, c.p3);
+      bf_finish<K>(x2, x3, t2, c.p3);
+      S::load(w, tww, j << (lq - s));
+      S::load(w2, tww, (j + h) << (lq - s));
+      mul_pm_lazy_dual<K>(t1, t2, x2, w, x3, w2, c.F.pm_c, c.F.pm_sh);
+      bf_finish<K>(x0, x2, t1, c.p3);
+      bf_finish<K>(x1, x3, t2, c.p3);
+    }
+    return;
+  }
+#endif
   if (trivial) {  // j == 0: the stage-s twiddle and the first stage-(s+1) twiddle are 1
     A::bf1(x0, x1, c);
     A::bf1(x2, x3, c);
