@@ -788,6 +788,138 @@ WM_DEV void mont_mul(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&
   select_n<K>(r, t[K] | (br ^ 0xffffffffu), d, lo);
 }
 
+// ------------------------------------------------------------------ paired products
+// Two independent products with their rows interleaved, for the NTT's paired
+// butterflies (WM_NTT_DUAL): the scheduler gets two dependency chains per
+// row instead of one (the pass kernels run at 4 warps per scheduler, so
+// per-thread ILP is what hides the multiply-add latency).
+
+// mul_shoup_lazy for (v1, w1, wp1) and (v2, w2, wp2).
+template <int K>
+WM_DEV void mul_shoup_lazy_dual(uint32_t (&r1)[K], uint32_t (&r2)[K], const uint32_t (&v1)[K],
+                                const uint32_t (&w1)[K], const uint32_t (&wp1)[K], const uint32_t (&v2)[K],
+                                const uint32_t (&w2)[K], const uint32_t (&wp2)[K], const uint32_t (&np)[K]) {
+  // high halves (columns >= K-2) of v*wp, compiler carries, interleaved
+  constexpr int C0 = (K > 2) ? K - 2 : 0;
+  constexpr int W = 2 * K - C0;
+  uint32_t h1[W], h2[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    h1[j] = 0u;
+    h2[j] = 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const int j0 = (C0 - i) > 0 ? (C0 - i) : 0;
+    uint32_t c1 = 0, c2 = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      if (j < j0) continue;
+      const uint64_t p1 = (uint64_t)v1[j] * wp1[i] + h1[i + j - C0] + c1;
+      const uint64_t p2 = (uint64_t)v2[j] * wp2[i] + h2[i + j - C0] + c2;
+      h1[i + j - C0] = (uint32_t)p1;
+      c1 = (uint32_t)(p1 >> 32);
+      h2[i + j - C0] = (uint32_t)p2;
+      c2 = (uint32_t)(p2 >> 32);
+    }
+    h1[i + K - C0] = c1;
+    h2[i + K - C0] = c2;
+  }
+  uint32_t q1[K], q2[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    q1[j] = h1[K - C0 + j];
+    q2[j] = h2[K - C0 + j];
+  }
+  // low halves: r = lo(v w) + lo(qh np), compiler carries, interleaved
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    r1[j] = 0u;
+    r2[j] = 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    uint32_t c1 = 0, c2 = 0, d1 = 0, d2 = 0;
+#pragma unroll
+    for (int j = 0; j + i < K - 1; ++j) {
+      const uint64_t p1 = (uint64_t)v1[j] * w1[i] + r1[i + j] + c1;
+      const uint64_t p2 = (uint64_t)v2[j] * w2[i] + r2[i + j] + c2;
+      r1[i + j] = (uint32_t)p1;
+      c1 = (uint32_t)(p1 >> 32);
+      r2[i + j] = (uint32_t)p2;
+      c2 = (uint32_t)(p2 >> 32);
+      const uint64_t s1 = (uint64_t)q1[j] * np[i] + r1[i + j] + d1;
+      const uint64_t s2 = (uint64_t)q2[j] * np[i] + r2[i + j] + d2;
+      r1[i + j] = (uint32_t)s1;
+      d1 = (uint32_t)(s1 >> 32);
+      r2[i + j] = (uint32_t)s2;
+      d2 = (uint32_t)(s2 >> 32);
+    }
+    r1[K - 1] += v1[K - 1 - i] * w1[i] + q1[K - 1 - i] * np[i] + c1 + d1;
+    r2[K - 1] += v2[K - 1 - i] * w2[i] + q2[K - 1 - i] * np[i] + c2 + d2;
+  }
+}
+
+// mont_mul for (a1, b1) and (a2, b2) (CIOS rows interleaved).
+template <int K>
+WM_DEV void mont_mul_dual(uint32_t (&r1)[K], uint32_t (&r2)[K], const uint32_t (&a1)[K], const uint32_t (&b1)[K],
+                          const uint32_t (&a2)[K], const uint32_t (&b2)[K], const uint32_t (&q)[K],
+                          uint32_t qinv) {
+  uint32_t t1[K + 2], t2[K + 2];
+#pragma unroll
+  for (int j = 0; j < K + 2; ++j) {
+    t1[j] = 0u;
+    t2[j] = 0u;
+  }
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    uint32_t c1 = 0, c2 = 0;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+      const uint64_t p1 = (uint64_t)a1[j] * b1[i] + t1[j] + c1;
+      const uint64_t p2 = (uint64_t)a2[j] * b2[i] + t2[j] + c2;
+      t1[j] = (uint32_t)p1;
+      c1 = (uint32_t)(p1 >> 32);
+      t2[j] = (uint32_t)p2;
+      c2 = (uint32_t)(p2 >> 32);
+    }
+    uint64_t s1 = (uint64_t)t1[K] + c1, s2 = (uint64_t)t2[K] + c2;
+    t1[K] = (uint32_t)s1;
+    t1[K + 1] = (uint32_t)(s1 >> 32);
+    t2[K] = (uint32_t)s2;
+    t2[K + 1] = (uint32_t)(s2 >> 32);
+    const uint32_t m1 = t1[0] * qinv, m2 = t2[0] * qinv;
+    uint64_t p1 = (uint64_t)m1 * q[0] + t1[0], p2 = (uint64_t)m2 * q[0] + t2[0];
+    c1 = (uint32_t)(p1 >> 32);
+    c2 = (uint32_t)(p2 >> 32);
+#pragma unroll
+    for (int j = 1; j < K; ++j) {
+      p1 = (uint64_t)m1 * q[j] + t1[j] + c1;
+      p2 = (uint64_t)m2 * q[j] + t2[j] + c2;
+      t1[j - 1] = (uint32_t)p1;
+      c1 = (uint32_t)(p1 >> 32);
+      t2[j - 1] = (uint32_t)p2;
+      c2 = (uint32_t)(p2 >> 32);
+    }
+    s1 = (uint64_t)t1[K] + c1;
+    s2 = (uint64_t)t2[K] + c2;
+    t1[K - 1] = (uint32_t)s1;
+    t1[K] = t1[K + 1] + (uint32_t)(s1 >> 32);
+    t2[K - 1] = (uint32_t)s2;
+    t2[K] = t2[K + 1] + (uint32_t)(s2 >> 32);
+  }
+  uint32_t lo1[K], lo2[K], d1[K], d2[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) {
+    lo1[j] = t1[j];
+    lo2[j] = t2[j];
+  }
+  const uint32_t br1 = sub_n<K>(d1, lo1, q);
+  const uint32_t br2 = sub_n<K>(d2, lo2, q);
+  select_n<K>(r1, t1[K] | (br1 ^ 0xffffffffu), d1, lo1);
+  select_n<K>(r2, t2[K] | (br2 ^ 0xffffffffu), d2, lo2);
+}
+
 // a b mod q for a full-width field by Barrett reduction (one product chain
 // instead of two Montgomery products).  The modulus is normalised to
 // qn = q << s with its top bit at 2^(M-1), M = 32K; mu = floor(2^(2M)/qn) =

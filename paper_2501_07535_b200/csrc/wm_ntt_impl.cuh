@@ -41,8 +41,9 @@
 
 // Minimum resident CTAs per SM requested from ptxas for the pass kernels
 // (caps registers at 65536 / (256 * WM_NTT_MINB)); A/B: tools/ab_timing.py.
-#ifndef WM_NTT_DUAL  // A/B: MODE 3 radix-4 groups with interleaved product pairs
-#define WM_NTT_DUAL 1  // 8.50 -> 8.34 us/transform (profiles/r02_ab_ntt_dual.txt)
+#ifndef WM_NTT_DUAL  // bit mask over arithmetic modes: radix-4 groups with interleaved product pairs
+#define WM_NTT_DUAL 10  // modes 3 and 1: 8.50 -> 8.34 (special form), 13.24 -> 13.08 us/transform
+                        // (BLS12-381 r); the Shoup modes 0/2 lose 2-4 % (profiles/r02_ab_ntt_dual*.txt)
 #endif
 #ifndef WM_NTT_MINB
 #define WM_NTT_MINB 2
@@ -124,6 +125,15 @@ struct Arith<K, 0> {
     bf_lazy<K>(x0, x1, w, wp, c.p3, c.np);
   }
   WM_DEV static void bf1(uint32_t (&x0)[K], uint32_t (&x1)[K], const NttConst<K> &c) { bf_lazy_w1<K>(x0, x1, c.p3); }
+  // two butterflies, products interleaved (WM_NTT_DUAL)
+  WM_DEV static void bf2(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&wp)[K],
+                         uint32_t (&y0)[K], uint32_t (&y1)[K], const uint32_t (&v)[K], const uint32_t (&vp)[K],
+                         const NttConst<K> &c) {
+    uint32_t t1[K], t2[K];
+    mul_shoup_lazy_dual<K>(t1, t2, x1, w, wp, y1, v, vp, c.np);
+    bf_finish<K>(x0, x1, t1, c.p3);
+    bf_finish<K>(y0, y1, t2, c.p3);
+  }
   WM_DEV static void twmul(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
                            const uint32_t (&wp)[K], const NttConst<K> &c) {
     mul_shoup_lazy<K>(r, v, w, wp, c.np);
@@ -154,6 +164,14 @@ struct Arith<K, 1> {
     uint32_t t[K];
     copy_n<K>(t, x1);
     finish(x0, x1, t, c);
+  }
+  WM_DEV static void bf2(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&)[K],
+                         uint32_t (&y0)[K], uint32_t (&y1)[K], const uint32_t (&v)[K], const uint32_t (&)[K],
+                         const NttConst<K> &c) {
+    uint32_t t1[K], t2[K];
+    mont_mul_dual<K>(t1, t2, x1, w, y1, v, c.p, c.F.qinv);
+    finish(x0, x1, t1, c);
+    finish(y0, y1, t2, c);
   }
   WM_DEV static void twmul(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
                            const uint32_t (&)[K], const NttConst<K> &c) {
@@ -189,6 +207,16 @@ struct Arith<K, 2> {
     copy_n<K>(t, x1);
     cond_sub<K>(t, c.p2);
     finish(x0, x1, t, c);
+  }
+  WM_DEV static void bf2(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&wp)[K],
+                         uint32_t (&y0)[K], uint32_t (&y1)[K], const uint32_t (&v)[K], const uint32_t (&vp)[K],
+                         const NttConst<K> &c) {
+    uint32_t t1[K], t2[K];
+    mul_shoup_lazy_dual<K>(t1, t2, x1, w, wp, y1, v, vp, c.np);  // [0, 3p)
+    cond_sub<K>(t1, c.p2);
+    cond_sub<K>(t2, c.p2);
+    finish(x0, x1, t1, c);
+    finish(y0, y1, t2, c);
   }
   WM_DEV static void twmul(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
                            const uint32_t (&wp)[K], const NttConst<K> &c) {
@@ -228,6 +256,14 @@ struct Arith<K, 3> {
     bf_finish<K>(x0, x1, t, c.p3);
   }
   WM_DEV static void bf1(uint32_t (&x0)[K], uint32_t (&x1)[K], const NttConst<K> &c) { bf_lazy_w1<K>(x0, x1, c.p3); }
+  WM_DEV static void bf2(uint32_t (&x0)[K], uint32_t (&x1)[K], const uint32_t (&w)[K], const uint32_t (&)[K],
+                         uint32_t (&y0)[K], uint32_t (&y1)[K], const uint32_t (&v)[K], const uint32_t (&)[K],
+                         const NttConst<K> &c) {
+    uint32_t t1[K], t2[K];
+    mul_pm_lazy_dual<K>(t1, t2, x1, w, y1, v, c.F.pm_c, c.F.pm_sh);
+    bf_finish<K>(x0, x1, t1, c.p3);
+    bf_finish<K>(y0, y1, t2, c.p3);
+  }
   WM_DEV static void twmul(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&w)[K],
                            const uint32_t (&)[K], const NttConst<K> &c) {
     mul_pm_lazy<K, pm_ntt_strat<K>()>(r, v, w, c.F.pm_c, c.F.pm_sh);
@@ -299,6 +335,17 @@ struct Smem {
   }
 };
 
+// Modes and limb counts whose radix-4 groups pair their products
+// (Arith::bf2); two products' working sets fit the 128-register budget of
+// 2 CTAs/SM up to 8 limbs.
+#ifndef WM_NTT_DUAL_MAXK
+#define WM_NTT_DUAL_MAXK 8
+#endif
+template <int K, int MODE>
+__host__ __device__ constexpr bool ntt_dual() {
+  return ((WM_NTT_DUAL >> MODE) & 1) && K <= WM_NTT_DUAL_MAXK;  // (radix-2 passes start at 24 limbs)
+}
+
 // ------------------------------------------------------------------ in-smem DFT
 // One radix-4 group (stages s, s+1) with one product at a time (wide K,
 // where two interleaved products would spill registers).
@@ -310,30 +357,24 @@ __device__ __forceinline__ void radix4_single(uint32_t (&x0)[K], uint32_t (&x1)[
   using S = Smem<K>;
   using A = Arith<K, MODE>;
   uint32_t w[K], wp[K];
-#if WM_NTT_DUAL
-  if constexpr (MODE == 3) {  // paired butterflies with interleaved products (A/B)
-    if (trivial) {
-      A::bf1(x0, x1, c);
-      A::bf1(x2, x3, c);
-      A::bf1(x0, x2, c);
-      const int i3 = (j + h) << (lq - s);
-      S::load(w, tww, i3);
-      A::bf(x1, x3, w, wp, c);
-    } else {
-      uint32_t t1[K], t2[K], w2[K];
-      S::load(w, tww, j << (logL - 1 - s));
-      mul_pm_lazy_dual<K>(t1, t2, x1, w, x3, w, c.F.pm_c, c.F.pm_sh);
-      bf_finish<K>(x0, x1, t1, c.p3);
-      bf_finish<K>(x2, x3, t2, c.p3);
-      S::load(w, tww, j << (lq - s));
-      S::load(w2, tww, (j + h) << (lq - s));
-      mul_pm_lazy_dual<K>(t1, t2, x2, w, x3, w2, c.F.pm_c, c.F.pm_sh);
-      bf_finish<K>(x0, x2, t1, c.p3);
-      bf_finish<K>(x1, x3, t2, c.p3);
+  if constexpr (ntt_dual<K, MODE>()) {  // paired butterflies, products interleaved
+    if (!trivial) {
+      uint32_t v[K], vp[K];
+      const int i1 = j << (logL - 1 - s);
+      S::load(w, tww, i1);
+      if constexpr (A::kWp) S::load(wp, twp, i1);
+      A::bf2(x0, x1, w, wp, x2, x3, w, wp, c);
+      const int i2 = j << (lq - s), i3 = (j + h) << (lq - s);
+      S::load(w, tww, i2);
+      S::load(v, tww, i3);
+      if constexpr (A::kWp) {
+        S::load(wp, twp, i2);
+        S::load(vp, twp, i3);
+      }
+      A::bf2(x0, x2, w, wp, x1, x3, v, vp, c);
+      return;
     }
-    return;
   }
-#endif
   if (trivial) {  // j == 0: the stage-s twiddle and the first stage-(s+1) twiddle are 1
     A::bf1(x0, x1, c);
     A::bf1(x2, x3, c);
