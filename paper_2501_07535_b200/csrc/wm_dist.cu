@@ -212,6 +212,7 @@ __global__ void twiddle_2d_kernel(uint32_t *table, int64_t n, int64_t row0, int6
 // 2^24 / P pairs (1 GiB / P).
 enum { kDistBarrett = 0, kDistMont = 1, kDistPm = 3 };
 
+
 // Full products of the special-form twiddle multiply: Karatsuba for 8..16
 // limbs as in the NTT passes (pm_ntt_strat), schoolbook elsewhere.
 template <int K>

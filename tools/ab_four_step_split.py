@@ -67,4 +67,4 @@ br = {"row_ntt_n2_ms": timed(lambda: b.row_ntt(x, L.n2, False)),
       "block_transpose_ms": timed(lambda: b.block_transpose(d, 1, L.n2, L.n1)),
       "row_ntt_n1_ms": timed(lambda: b.row_ntt(e, L.n1, False)),
       "total_ms": timed(lambda: eng.forward(x))}
-print(json.dumps({"breakdown_4096x4096": {k: round(v, 4) for k, v in br.items()}}))
+print(json.dumps({f"breakdown_{L.n1}x{L.n2}": {k: round(v, 4) for k, v in br.items()}}))
