@@ -30,6 +30,23 @@ def test_shard_range():
             assert max(sizes) - min(sizes) <= 1
 
 
+def test_split_lengths():
+    """Balanced split by default; with the limb count, n >= 2^20 at <= 12 limbs
+    puts one 1024-point pass on each phase-1 row (dist.split_lengths)."""
+    assert D.split_lengths(1 << 10) == (32, 32)
+    assert D.split_lengths(1 << 11) == (64, 32)
+    assert D.split_lengths(1 << 24) == (4096, 4096)
+    assert D.split_lengths(1 << 24, 8) == (16384, 1024)
+    assert D.split_lengths(1 << 20, 12) == (1024, 1024)
+    assert D.split_lengths(1 << 24, 24) == (4096, 4096)
+    assert D.split_lengths(1 << 16, 8) == (256, 256)
+    for n in (1 << 20, 1 << 22, 1 << 24, 1 << 26):
+        n1, n2 = D.split_lengths(n, 8)
+        assert n1 * n2 == n and n1 >= n2
+    with pytest.raises(ValueError):
+        D.split_lengths(3)
+
+
 def test_layout_maps_roundtrip():
     n = 1 << 10
     L = D.FourStepLayout(n, *D.split_lengths(n), 4)
