@@ -683,10 +683,22 @@ def run_four_step_fused(torch, prm, rank, world, pg, x, y_ref, reps):
             own_group = True
         n = prm.n
         comm = D.SymmComm(n // world * K_LIMBS)
-        eng = D.FourStepNtt(BITS, prm, rank, world, comm=comm)
-        y = eng.forward(x)
-        torch.cuda.synchronize()
-        ok = bool(torch.equal(y, y_ref)) and bool(torch.equal(eng.inverse(y), x))
+        err = None
+        try:
+            eng = D.FourStepNtt(BITS, prm, rank, world, comm=comm)
+            y = eng.forward(x)
+            torch.cuda.synchronize()
+            ok = bool(torch.equal(y, y_ref)) and bool(torch.equal(eng.inverse(y), x))
+        except Exception as exc:  # noqa: BLE001 - agreed on below
+            err = exc
+        # every rank learns whether any rank failed before the timing collectives
+        if pg is not None:  # pg is the torch.distributed module (dist_setup)
+            flag = torch.tensor([0 if err is None else 1], dtype=torch.int32, device="cuda")
+            pg.all_reduce(flag, op=pg.ReduceOp.MAX)
+            if int(flag.item()) and err is None:
+                err = RuntimeError("fused four-step failed on another rank")
+        if err is not None:
+            raise err
         stream = torch.cuda.current_stream()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier(pg)
