@@ -723,6 +723,25 @@ WM_DEV void mul_pm_lazy_dual(uint32_t (&r1)[K], uint32_t (&r2)[K], const uint32_
   pm_reduce_wide<K>(r2, t2, c, sh);
 }
 
+// [0, 8q) -> [0, q) for special-form q = 2^m - c: with k = v >> m (< 8),
+// v - k q = (v mod 2^m) + k c < 2^m + 7c < 2q (m >= 72), so one conditional
+// subtraction finishes (one small product + one carry chain instead of three
+// conditional subtractions).
+template <int K>
+WM_DEV void pm_canonical(uint32_t (&v)[K], const uint32_t (&q)[K], uint32_t c, uint32_t sh) {
+  const uint32_t rs = 32u - sh;                // m mod 32
+  const uint32_t k = v[K - 1] >> rs;           // v >> m
+  const uint64_t kc = (uint64_t)k * c;         // < 2^35
+  uint32_t add[K];
+  add[0] = (uint32_t)kc;
+  add[1] = (uint32_t)(kc >> 32);
+#pragma unroll
+  for (int j = 2; j < K; ++j) add[j] = 0u;
+  v[K - 1] &= 0xffffffffu >> sh;               // v mod 2^m
+  add_n<K>(v, v, add);
+  cond_sub<K>(v, q);
+}
+
 // Canonical special-form product of canonical a, b.
 template <int K, int STRAT = kSchoolbook>
 WM_DEV void mul_pm(uint32_t (&r)[K], const uint32_t (&a)[K], const uint32_t (&b)[K], const FieldConst<K> &F) {

@@ -45,6 +45,9 @@
 #define WM_NTT_DUAL 10  // modes 3 and 1: 8.50 -> 8.34 (special form), 13.24 -> 13.08 us/transform
                         // (BLS12-381 r); the Shoup modes 0/2 lose 2-4 % (profiles/r02_ab_ntt_dual*.txt)
 #endif
+#ifndef WM_PM_CANON  // special-form fields: canonicalise [0, 6p) by the top bits (A/B)
+#define WM_PM_CANON 1  // row pass 243.6 -> 238.6 us, 8.32 -> 8.25 us/transform (profiles/r02_ab_pm_canon.txt)
+#endif
 #ifndef WM_NTT_MINB
 #define WM_NTT_MINB 2
 #endif
@@ -268,7 +271,13 @@ struct Arith<K, 3> {
                            const uint32_t (&)[K], const NttConst<K> &c) {
     mul_pm_lazy<K, pm_ntt_strat<K>()>(r, v, w, c.F.pm_c, c.F.pm_sh);
   }
-  WM_DEV static void canon(uint32_t (&v)[K], const NttConst<K> &c) { canonical_6p<K>(v, c.p, c.p2, c.p4); }
+  WM_DEV static void canon(uint32_t (&v)[K], const NttConst<K> &c) {
+#if WM_PM_CANON
+    pm_canonical<K>(v, c.p, c.F.pm_c, c.F.pm_sh);
+#else
+    canonical_6p<K>(v, c.p, c.p2, c.p4);
+#endif
+  }
   WM_DEV static void mulby(uint32_t (&r)[K], const uint32_t (&v)[K], const uint32_t (&m)[K], const NttConst<K> &c) {
     mul_pm<K>(r, v, m, c.F);
   }
