@@ -256,6 +256,53 @@ def build_program(spec: KernelSpec, params_mode: str = "baked") -> DeviceKernel:
     return DeviceKernel(spec, params_mode)
 
 
+def _check_params_mode(params_mode: str) -> None:
+    if params_mode not in PARAMS_MODES:
+        raise InvalidKernel(f"unknown params mode {params_mode!r}")
+
+
+def build_scalar(kind: str, layout: WordLayout, barrett: BarrettParams,
+                 params_mode: str = "baked") -> DeviceKernel:
+    """addmod / submod / mulmod on one element (reference kernels.py:184-212).
+    ``run_program`` executes it on the device."""
+    if kind not in SCALAR_KINDS:
+        raise InvalidKernel(f"not a scalar kernel: {kind!r}")
+    _check_params_mode(params_mode)
+    return DeviceKernel(KernelSpec(kind, layout, 1, barrett), params_mode)
+
+
+def build_vector(kind: str, layout: WordLayout, size: int, barrett: BarrettParams,
+                 params_mode: str = "baked") -> DeviceKernel:
+    """Elementwise vadd / vsub / vmul / axpy over ``size`` elements (reference
+    kernels.py:215-256); ``run_vector`` executes it on the device."""
+    if kind not in VECTOR_KINDS:
+        raise InvalidKernel(f"not a vector kernel: {kind!r}")
+    if size < 1:
+        raise InvalidKernel("vector size must be positive")
+    _check_params_mode(params_mode)
+    return DeviceKernel(KernelSpec(kind, layout, size, barrett), params_mode)
+
+
+def build_ntt(kind: str, layout: WordLayout, params: NttParams,
+              params_mode: str = "baked") -> DeviceKernel:
+    """Forward / inverse transform over ``params`` (reference kernels.py:270-311;
+    the reference builds one butterfly plus schedule data, the device handle
+    runs whole transforms through ``run_ntt`` and single butterflies through
+    ``run_program``)."""
+    if kind not in NTT_KINDS:
+        raise InvalidKernel(f"not a transform kernel: {kind!r}")
+    _check_params_mode(params_mode)
+    if params.n < 2 or params.n & (params.n - 1):
+        raise InvalidKernel(f"transform length {params.n} is not a power of two at least 2")
+    barrett = compute_barrett(params.p, layout.bits)
+    return DeviceKernel(KernelSpec(kind, layout, params.n, barrett, params), params_mode)
+
+
+def build_wide_mul(layout: WordLayout) -> DeviceKernel:
+    """Bare widening multiply a * b -> 2 x width (reference kernels.py:314-329)."""
+    return DeviceKernel(KernelSpec("widemul", layout), "baked")
+
+
 def generate_kernel(spec: KernelSpec, params_mode: str = "baked", target_has_double_word: bool = True,
                     prune: bool = True, trace: list | None = None) -> DeviceKernel:
     """Reference kernels.py:368-381.  The lowering/pruning the reference does
