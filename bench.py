@@ -486,6 +486,16 @@ def run_blas(args, torch, _field, rank, world, pg):
                 row = {"op": op, "bits": bits, "n": n, "ms": round(ms, 4), "GB_per_s": round(gbs, 1),
                        "hbm_frac_of_measured": round(gbs / (world * hbm), 3), "strategy": fm.strategy,
                        "reduction": fm.reduction if op != "vadd" else None}
+                # binding roofline: the slower of HBM traffic and the
+                # executed word products (wm_blas_work) at the measured product peak
+                wp = fm.work(op)
+                if wp:
+                    t_int = wp * n / (world * int_peak_wmul_per_s()[0])
+                    t_hbm = 3 * 4 * K * n / (world * hbm * 1e9)
+                    row.update(word_products_per_elem=wp,
+                               int_frac_executed=round(t_int / (ms * 1e-3), 3),
+                               binding="int" if t_int > t_hbm else "hbm",
+                               binding_frac=round(max(t_int, t_hbm) / (ms * 1e-3), 3))
                 out_rows.append(row)
         # parity of the benchmarked slice (both reductions, all ops) against each other
         # is in tests/test_reduction_gpu.py; here a cheap cross-check of the last one
@@ -495,7 +505,10 @@ def run_blas(args, torch, _field, rank, world, pg):
     return {"rows": out_rows, "hbm_measured_gbs": hbm, "ranks": world,
             "sharding": f"contiguous n/{world} slice per rank, no collective; ms = max over ranks",
             "note": "median of 10 launches; operands 0.8-4.8 GB (> L2); bytes = 2 reads + 1 write per element; "
-                    "hbm_frac_of_measured = GB/s / (ranks x measured HBM copy bandwidth)"}
+                    "hbm_frac_of_measured = GB/s / (ranks x measured HBM copy bandwidth); vmul/axpy rows: "
+                    "int_frac_executed = word products per element (wm_blas_work) x n / time / (ranks x measured "
+                    "product peak), binding = the larger of the HBM and product times, binding_frac = that time "
+                    "/ measured time"}
 
 
 def run_drop_in(args, torch):

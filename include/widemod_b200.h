@@ -275,10 +275,16 @@ int wm_scale_transpose_fx(const wm_field *f, const uint32_t *in, const uint32_t 
  *   wm_ntt_pass_work: field multiplications the pass kernel `pass_index` of a
  *     forward (inverse != 0: inverse) transform executes for `batch`
  *     transforms, and the word products they cost in the plan's arithmetic
- *     (32x32->32 low products count one half). */
+ *     (32x32->32 low products count one half).
+ *   wm_blas_work: the same per element of a BLAS op. */
 int wm_probe_imad_wide(int mode, int64_t iters, uint64_t *sink, void *stream, int64_t *products);
 int wm_ntt_pass_work(const wm_ntt_plan *p, int inverse, int pass_index, int64_t batch, int64_t *field_muls,
                      double *word_products);
+/* Word products one element of `op` (WM_OP_*) executes in the field's
+ * arithmetic (mirrors the BLAS templates: Karatsuba levels, truncated Barrett
+ * quotient, or the special-form folds; a 32x32->32 low product counts one
+ * half; 0 for vadd/vsub).  WM_EUNSUPPORTED for Montgomery fields. */
+int wm_blas_work(const wm_field *f, int op, double *word_products);
 
 /* ---------------------------------------------------------------- layout
  * Reference layout: AoS, `ref_words` words of `word_bits` (32 or 64) per

@@ -82,6 +82,7 @@ SIGNATURES = [
                                      _vp]),
     ("wm_probe_imad_wide", _int, [_int, _i64, _vp, _vp, ctypes.POINTER(_i64)]),
     ("wm_ntt_pass_work", _int, [_vp, _int, _int, _i64, ctypes.POINTER(_i64), ctypes.POINTER(ctypes.c_double)]),
+    ("wm_blas_work", _int, [_vp, _int, ctypes.POINTER(ctypes.c_double)]),
     ("wm_ref_to_limbs", _int, [_int, _int, _int, _vp, _vp, _i64, _vp]),
     ("wm_limbs_to_ref", _int, [_int, _int, _int, _vp, _vp, _i64, _vp]),
 ]

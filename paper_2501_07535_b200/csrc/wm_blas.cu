@@ -235,6 +235,126 @@ __global__ void __launch_bounds__(256, (K > 24 ? WM_BLAS_MINB_HUGE : K >= 16 ? W
   }
 }
 
+// ------------------------------------------------------------------ TMA-staged heavy ops
+// vmul/axpy from 8 limbs are integer-bound per element, and in the plain
+// grid-stride kernel each thread issues its next loads only after the current
+// element's multiply: at 2 CTAs/SM the loads and the products take turns
+// (256-bit Barrett vmul and 768-bit special-form vmul both ran at ~0.5-0.6 of
+// their HBM and product rooflines).  Here a persistent CTA streams tiles of
+// 256 elements through a WM_BLAS_TMA_STAGES-deep shared-memory ring: one
+// thread refills a stage with two TMA bulk copies (cp.async.bulk, completion
+// counted on the stage's mbarrier) as soon as every thread has read it, so
+// the operands of the next tiles arrive while the current tile is multiplied.
+#ifndef WM_BLAS_TMA
+#define WM_BLAS_TMA 1
+#endif
+#ifndef WM_BLAS_TMA_STAGES
+#define WM_BLAS_TMA_STAGES 2
+#endif
+constexpr int kTmaTile = 256;
+
+#ifndef WM_BLAS_TMA_MINK
+#define WM_BLAS_TMA_MINK 24
+#endif
+// Where it is used: the generic Barrett multiply from 24 limbs.  Measured
+// against the plain kernel at every width (profiles/r02_ab_blas_tma_all.txt,
+// r02_ab_blas_tma_wide.txt): 768-bit Barrett vmul/axpy +15 % / +10 %,
+// 1024-bit +5..13 % (axpy Karatsuba -4 %), but 256/384/512-bit Barrett
+// -3..7 % and the special-form multiplies -6..+3 % (their loads already
+// overlap the products: more resident warps, or HBM-bound).
+template <int K, int STRAT>
+constexpr bool blas_tma_k() {
+  return WM_BLAS_TMA && K >= WM_BLAS_TMA_MINK && K % 4 == 0 && (STRAT == kSchoolbook || STRAT == kKaratsuba);
+}
+
+template <int K>
+constexpr size_t blas_tma_smem() {
+  return (size_t)WM_BLAS_TMA_STAGES * 2 * kTmaTile * K * sizeof(uint32_t) + WM_BLAS_TMA_STAGES * sizeof(uint64_t);
+}
+
+WM_DEV uint32_t blas_smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+WM_DEV void blas_tma_fill(uint32_t *dst_a, uint32_t *dst_b, const uint32_t *src_a, const uint32_t *src_b,
+                          uint32_t bytes, uint64_t *mbar) {
+  const uint32_t mb = blas_smem_addr(mbar);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // this stage's generic reads before the refill
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mb), "r"(2 * bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(blas_smem_addr(dst_a)), "l"(src_a), "r"(bytes), "r"(mb)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(blas_smem_addr(dst_b)), "l"(src_b), "r"(bytes), "r"(mb)
+               : "memory");
+}
+
+WM_DEV void blas_tma_wait(uint64_t *mbar, uint32_t parity) {
+  const uint32_t mb = blas_smem_addr(mbar);
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(mb), "r"(parity)
+        : "memory");
+  }
+}
+
+template <int K, int OP, int STRAT>
+__global__ void __launch_bounds__(256, (K > 24 ? WM_BLAS_MINB_HUGE : K >= 16 ? WM_BLAS_MINB_WIDE : K >= 9 ? WM_BLAS_MINB_MID : 1))
+    blas_tma_kernel(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n,
+                    const __grid_constant__ BlasArgs<K> args) {
+  constexpr int T = kTmaTile, S = WM_BLAS_TMA_STAGES;
+  constexpr uint32_t TILE = T * K;  // words per operand tile
+  extern __shared__ __align__(128) uint32_t sm[];  // [S][a|b][T*K], then S mbarriers
+  uint64_t *bar = reinterpret_cast<uint64_t *>(sm + S * 2 * TILE);
+  const int64_t tiles = n / T, step = gridDim.x;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(blas_smem_addr(&bar[s])) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      const int64_t t = blockIdx.x + s * step;
+      if (t < tiles)
+        blas_tma_fill(sm + (2 * s) * TILE, sm + (2 * s + 1) * TILE, a + t * TILE, b + t * TILE, TILE * 4, &bar[s]);
+    }
+  }
+  __syncthreads();
+  int j = 0;
+#pragma unroll 1
+  for (int64_t t = blockIdx.x; t < tiles; t += step, ++j) {
+    const int s = j % S;
+    blas_tma_wait(&bar[s], (uint32_t)(j / S) & 1u);
+    uint32_t x[K], y[K], r[K];
+    const uint4 *xs = reinterpret_cast<const uint4 *>(sm + (2 * s) * TILE + threadIdx.x * K);
+    const uint4 *ys = reinterpret_cast<const uint4 *>(sm + (2 * s + 1) * TILE + threadIdx.x * K);
+#pragma unroll
+    for (int c = 0; c < K / 4; ++c) {
+      const uint4 u = xs[c], v = ys[c];
+      x[4 * c] = u.x; x[4 * c + 1] = u.y; x[4 * c + 2] = u.z; x[4 * c + 3] = u.w;
+      y[4 * c] = v.x; y[4 * c + 1] = v.y; y[4 * c + 2] = v.z; y[4 * c + 3] = v.w;
+    }
+    __syncthreads();  // stage s is read: refill it with tile t + S * step
+    if (threadIdx.x == 0) {
+      const int64_t nt = t + S * step;
+      if (nt < tiles)
+        blas_tma_fill(sm + (2 * s) * TILE, sm + (2 * s + 1) * TILE, a + nt * TILE, b + nt * TILE, TILE * 4, &bar[s]);
+    }
+    blas_elem<K, OP, STRAT>(r, x, y, args);
+    store_elem<K>(out, t * T + threadIdx.x, r);
+  }
+  // the last n mod T elements: direct loads
+  for (int64_t i = tiles * T + (int64_t)blockIdx.x * T + threadIdx.x; i < n; i += step * T) {
+    uint32_t x[K], y[K], r[K];
+    load_elem<K>(x, a, i);
+    load_elem<K>(y, b, i);
+    blas_elem<K, OP, STRAT>(r, x, y, args);
+    store_elem<K>(out, i, r);
+  }
+}
+
 #ifndef WM_BLAS_SMALL_WORDWISE
 #define WM_BLAS_SMALL_WORDWISE 1
 #endif
@@ -291,6 +411,27 @@ static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, 
     const Big a(scal_host, scal_host + K);
     const Big sh = f->mont ? to_mont(a, f->q) : (STRAT == kPmField || STRAT == kPmKara) ? a : big_shl(a, f->s, K);
     for (int j = 0; j < K; ++j) args.scal[j] = sh[j];
+  }
+  if constexpr (blas_tma_k<K, STRAT>() && (OP == OP_VMUL || OP == OP_AXPY)) {
+    // TMA needs 16-byte aligned sources (element views of cudaMalloc'd
+    // buffers always are for 4 | K); a persistent grid of resident CTAs
+    if ((((uintptr_t)a | (uintptr_t)b) & 15) == 0 && n >= kTmaTile) {
+      static std::atomic<int> tocc[64];
+      constexpr size_t smem = blas_tma_smem<K>();
+      int tb = tocc[dev & 63].load(std::memory_order_relaxed);
+      if (tb == 0) {
+        WM_CUDA_TRY(cudaFuncSetAttribute(blas_tma_kernel<K, OP, STRAT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem));
+        WM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&tb, blas_tma_kernel<K, OP, STRAT>, 256, smem));
+        tb = std::max(1, tb);
+        tocc[dev & 63].store(tb, std::memory_order_relaxed);
+      }
+      const int64_t tiles = n / kTmaTile;
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)sm_count * tb));
+      blas_tma_kernel<K, OP, STRAT><<<grid, 256, smem, st>>>(a, b, out, n, args);
+      WM_LAUNCH_CHECK("blas_tma_kernel launch");
+      return WM_OK;
+    }
   }
   int64_t want = (n + 255) / 256;
 #ifndef WM_BLAS_WAVES  // grid cap in waves of resident CTAs (0: one thread per element)
@@ -464,6 +605,10 @@ static void preload_blas_k() {
   (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_VSUB, STRAT == kMontField ? kMontField : kSchoolbook>);
   (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_VMUL, STRAT>);
   (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_AXPY, STRAT>);
+  if constexpr (blas_tma_k<K, STRAT>()) {
+    (void)cudaFuncGetAttributes(&a, (const void *)blas_tma_kernel<K, OP_VMUL, STRAT>);
+    (void)cudaFuncGetAttributes(&a, (const void *)blas_tma_kernel<K, OP_AXPY, STRAT>);
+  }
 }
 
 void preload_field(const wm_field *f) {

@@ -127,3 +127,34 @@ extern "C" int wm_ntt_pass_work(const wm_ntt_plan *p, int inverse, int pass_inde
   if (word_products) *word_products = (double)muls * (double)half_products_per_mul(p) / 2.0;
   return WM_OK;
 }
+
+// Word products of one K x K full product as mul_full_s forms it: Karatsuba
+// levels while the limb count is even and >= 4, recursing into halves that
+// are even and >= 8 limbs (WM_KARA_REC_MIN), schoolbook K^2 otherwise.
+static int64_t full_products(int K, bool kara) {
+  if (!kara || K % 2 || K < 4) return (int64_t)K * K;
+  const int H = K / 2;
+  return 3 * ((H >= 8 && H % 2 == 0) ? full_products(H, true) : (int64_t)H * H);
+}
+
+extern "C" int wm_blas_work(const wm_field *f, int op, double *word_products) {
+  if (!f) return fail(WM_EINVAL, "null field");
+  if (op < WM_OP_VADD || op > WM_OP_AXPY) return fail(WM_EINVAL, "bad op");
+  if (!word_products) return fail(WM_EINVAL, "null output");
+  if (op == WM_OP_VADD || op == WM_OP_VSUB) {
+    *word_products = 0.0;
+    return WM_OK;
+  }
+  if (f->mont) return fail(WM_EUNSUPPORTED, "the work model covers Barrett and special-form fields");
+  const int64_t K = f->K;
+  const int64_t full = full_products(f->K, f->karatsuba);
+  int64_t halves;
+  if (f->pm) {  // mul_pm: full product + two folds (K + 2 products)
+    halves = 2 * (full + K + 2);
+  } else {      // mul_barrett_pre: full + truncated high half (D = 2) + low half (K(K-1)/2 wide + K lo)
+    const int64_t C0 = K > 2 ? K - 2 : 0;
+    halves = 2 * (full + K * K - C0 * (C0 + 1) / 2) + 2 * (K * (K - 1) / 2) + K;
+  }
+  *word_products = (double)halves / 2.0;
+  return WM_OK;
+}

@@ -232,6 +232,18 @@ class Field:
                                          _stream_ptr(stream)), "wm_blas_host")
         return out_host
 
+    def work(self, kind: str) -> float:
+        """Word products one element of `kind` executes in this field's
+        arithmetic (wm_blas_work): the executed-work basis of the BLAS
+        integer roofline."""
+        codes = {"vadd": _lib.WM_OP_VADD, "vsub": _lib.WM_OP_VSUB, "vmul": _lib.WM_OP_VMUL,
+                 "axpy": _lib.WM_OP_AXPY}
+        if kind not in codes:
+            raise ValueError(f"bad kind {kind!r}")
+        wp = ctypes.c_double()
+        _lib.check(self.lib.wm_blas_work(self._h, codes[kind], ctypes.byref(wp)), "wm_blas_work")
+        return wp.value
+
     # ---------------------------------------------------------------- layout
     def from_ref_layout(self, ref, word_bits: int, ref_words: int, out=None, stream=None):
         """Reference AoS MSW-first words (kernels.to_words) -> limb tensor."""

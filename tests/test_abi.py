@@ -100,3 +100,26 @@ def test_full_width_and_padded_field_creation(lib):
     assert k.value == 24
     lib.wm_field_destroy(h)
     assert lib.wm_field_create_ex(640, _limbs(q640 + 1, 20), 20, 0, ctypes.byref(h)) == _lib.WM_EUNSUPPORTED
+
+
+def test_blas_work_model(lib):
+    """wm_blas_work (host only): word products per element in each field
+    arithmetic, against hand counts of the templates in wm_limb.cuh."""
+    def work(bits, q, flags, op):
+        k = lib.wm_limbs_for_bits(bits)
+        h = ctypes.c_void_p()
+        assert lib.wm_field_create_ex(bits, _limbs(q, k), k, flags, ctypes.byref(h)) == _lib.WM_OK
+        wp = ctypes.c_double()
+        rc = lib.wm_blas_work(h, op, ctypes.byref(wp))
+        lib.wm_field_destroy(h)
+        return rc, wp.value
+
+    KA, BA, MO = 1, 4, 2  # WM_FIELD_KARATSUBA / BARRETT / MONTGOMERY
+    q256, q768 = (1 << 252) - 129, (1 << 764) - 393
+    assert work(256, q256, 0, _lib.WM_OP_VADD) == (0, 0.0)
+    assert work(256, q256, 0, _lib.WM_OP_VMUL) == (0, 64 + 8 + 2)          # schoolbook + two folds
+    assert work(256, q256, KA, _lib.WM_OP_AXPY) == (0, 48 + 8 + 2)         # one Karatsuba level
+    assert work(256, q256, KA | BA, _lib.WM_OP_VMUL) == (0, 48 + 43 + 28 + 4)  # Barrett: full + hi + lo
+    assert work(768, q768, KA, _lib.WM_OP_VMUL) == (0, 324 + 24 + 2)       # two Karatsuba levels
+    assert work(768, q768, KA | BA, _lib.WM_OP_VMUL) == (0, 324 + 323 + 276 + 12)
+    assert work(256, (1 << 255) - 19, MO, _lib.WM_OP_VMUL)[0] == _lib.WM_EUNSUPPORTED

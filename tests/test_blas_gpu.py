@@ -251,3 +251,32 @@ def test_small_elements_packed_and_unaligned(cuda, bits, offset):
                        ("axpy", [(s * u + v) % q for u, v in zip(a, b)])):
         r = f.axpy(s, x, y, out=out) if kind == "axpy" else getattr(f, kind)(x, y, out=out)
         assert dev.limbs_to_ints(dev.to_host(r)) == want, (kind, bits, offset)
+
+
+@pytest.mark.parametrize("bits,strategy", [(768, "karatsuba"), (768, "schoolbook"), (1024, "karatsuba")])
+def test_tma_staged_barrett_path(cuda, bits, strategy):
+    """The TMA-staged kernel (generic Barrett vmul/axpy from 24 limbs):
+    several tiles per CTA (stage reuse, both mbarrier phases), a ragged tail
+    of n mod 256 elements, an element-offset view, and out aliasing an
+    input, all against Python ints."""
+    import torch
+    dev = _dev()
+    from paper_2501_07535_b200.params import find_ntt_params
+    q = find_ntt_params(bits, 1).p
+    f = dev.Field(bits, q, strategy, reduction="barrett")
+    r = random.Random(bits)
+    n = 256 * 700 + 77
+    xs = [r.randrange(q) for _ in range(n + 1)]
+    ys = [r.randrange(q) for _ in range(n)]
+    ys[:3] = [0, 1, q - 1]
+    xs[1:4] = [q - 1, q - 1, 0]
+    xd = dev.to_device(dev.ints_to_limbs(xs, f.limbs))[1:]  # element-offset view
+    yd = dev.to_device(dev.ints_to_limbs(ys, f.limbs))
+    want = [a * b % q for a, b in zip(xs[1:], ys)]
+    assert dev.limbs_to_ints(dev.to_host(f.vmul(xd, yd))) == want
+    a = r.randrange(q)
+    want_axpy = [(a * x + y) % q for x, y in zip(xs[1:], ys)]
+    y2 = yd.clone()
+    f.axpy(a, xd, y2, out=y2)  # out aliases y
+    assert dev.limbs_to_ints(dev.to_host(y2)) == want_axpy
+    torch.cuda.synchronize()
