@@ -574,18 +574,29 @@ __host__ __device__ constexpr int barrett_style() {
 template <int K, int ST = barrett_style<K>(), int STRAT = kSchoolbook>
 WM_DEV void mul_barrett_pre(uint32_t (&r)[K], const uint32_t (&a_shifted)[K], const uint32_t (&b)[K],
                             const FieldConst<K> &F) {
+  // Carry style per product (A/B of every mix, profiles/r02_ab_barrett_style_mix.txt):
+  // a Karatsuba full product takes compiler carries at any width (768-bit
+  // vmul/axpy +7 % / +5 % over PTX chains); the quotient's high and low
+  // products keep the width's style.  WM_BARRETT_MIX (bit 0/1/2 = PTX chains
+  // for the full / high / low product) overrides for experiments.
+#ifndef WM_BARRETT_MIX
+#define WM_BARRETT_MIX -1
+#endif
+  constexpr int S0 = WM_BARRETT_MIX >= 0 ? ((WM_BARRETT_MIX & 1) ? kPtx : kU64) : (STRAT == kKaratsuba ? kU64 : ST);
+  constexpr int S1 = WM_BARRETT_MIX >= 0 ? ((WM_BARRETT_MIX & 2) ? kPtx : kU64) : ST;
+  constexpr int S2 = WM_BARRETT_MIX >= 0 ? ((WM_BARRETT_MIX & 4) ? kPtx : kU64) : ST;
   uint32_t t[2 * K];
-  mul_full_s<K, ST, STRAT>(t, a_shifted, b);
+  mul_full_s<K, S0, STRAT>(t, a_shifted, b);
   // q1 = t >> (M - 1) = t >> (32K - 5): limbs K-1 .. 2K-1 shifted by 27.
   uint32_t q1[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) q1[j] = __funnelshift_r(t[K - 1 + j], (j + K < 2 * K) ? t[K + j] : 0u, 27);
   uint32_t q3[K];
-  mul_hi_trunc<K, ST>(q3, q1, F.mu8);
+  mul_hi_trunc<K, S1>(q3, q1, F.mu8);
   uint32_t rr[K];
 #pragma unroll
   for (int j = 0; j < K; ++j) rr[j] = t[j];
-  mul_lo_acc<K, ST>(rr, q3, F.nqn);
+  mul_lo_acc<K, S2>(rr, q3, F.nqn);
   cond_sub<K>(rr, F.qn2);
   cond_sub<K>(rr, F.qn);
   shr_small<K>(r, rr, F.s);
