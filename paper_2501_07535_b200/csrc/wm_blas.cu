@@ -256,15 +256,18 @@ constexpr int kTmaTile = 256;
 #ifndef WM_BLAS_TMA_MINK
 #define WM_BLAS_TMA_MINK 24
 #endif
-// Where it is used: the generic Barrett multiply from 24 limbs.  Measured
-// against the plain kernel at every width (profiles/r02_ab_blas_tma_all.txt,
-// r02_ab_blas_tma_wide.txt): 768-bit Barrett vmul/axpy +15 % / +10 %,
-// 1024-bit +5..13 % (axpy Karatsuba -4 %), but 256/384/512-bit Barrett
-// -3..7 % and the special-form multiplies -6..+3 % (their loads already
-// overlap the products: more resident warps, or HBM-bound).
-template <int K, int STRAT>
+// Where it is used: the generic Barrett multiply from 24 limbs, and the
+// 256-bit special-form axpy.  Measured against the plain kernel at every
+// width (profiles/r02_ab_blas_tma_all.txt, r02_ab_blas_tma_wide.txt):
+// 768-bit Barrett vmul/axpy +15 % / +10 %, 1024-bit +5..13 % (axpy
+// Karatsuba -4 %), 256-bit special-form axpy +4 %, but 256/384/512-bit
+// Barrett -3..7 % and the other special-form multiplies -6..+3 % (their
+// loads already overlap the products: more resident warps, or HBM-bound).
+template <int K, int STRAT, int OP>
 constexpr bool blas_tma_k() {
-  return WM_BLAS_TMA && K >= WM_BLAS_TMA_MINK && K % 4 == 0 && (STRAT == kSchoolbook || STRAT == kKaratsuba);
+  if constexpr (!WM_BLAS_TMA || K % 4 != 0 || (OP != OP_VMUL && OP != OP_AXPY)) return false;
+  if constexpr (STRAT == kSchoolbook || STRAT == kKaratsuba) return K >= WM_BLAS_TMA_MINK;
+  return (STRAT == kPmField || STRAT == kPmKara) && K == 8 && OP == OP_AXPY;
 }
 
 template <int K>
@@ -412,7 +415,7 @@ static int launch_blas(const wm_field *f, const uint32_t *a, const uint32_t *b, 
     const Big sh = f->mont ? to_mont(a, f->q) : (STRAT == kPmField || STRAT == kPmKara) ? a : big_shl(a, f->s, K);
     for (int j = 0; j < K; ++j) args.scal[j] = sh[j];
   }
-  if constexpr (blas_tma_k<K, STRAT>() && (OP == OP_VMUL || OP == OP_AXPY)) {
+  if constexpr (blas_tma_k<K, STRAT, OP>()) {
     // TMA needs 16-byte aligned sources (element views of cudaMalloc'd
     // buffers always are for 4 | K); a persistent grid of resident CTAs
     if ((((uintptr_t)a | (uintptr_t)b) & 15) == 0 && n >= kTmaTile) {
@@ -605,10 +608,10 @@ static void preload_blas_k() {
   (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_VSUB, STRAT == kMontField ? kMontField : kSchoolbook>);
   (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_VMUL, STRAT>);
   (void)cudaFuncGetAttributes(&a, (const void *)blas_kernel<K, OP_AXPY, STRAT>);
-  if constexpr (blas_tma_k<K, STRAT>()) {
+  if constexpr (blas_tma_k<K, STRAT, OP_VMUL>())
     (void)cudaFuncGetAttributes(&a, (const void *)blas_tma_kernel<K, OP_VMUL, STRAT>);
+  if constexpr (blas_tma_k<K, STRAT, OP_AXPY>())
     (void)cudaFuncGetAttributes(&a, (const void *)blas_tma_kernel<K, OP_AXPY, STRAT>);
-  }
 }
 
 void preload_field(const wm_field *f) {

@@ -253,17 +253,19 @@ def test_small_elements_packed_and_unaligned(cuda, bits, offset):
         assert dev.limbs_to_ints(dev.to_host(r)) == want, (kind, bits, offset)
 
 
-@pytest.mark.parametrize("bits,strategy", [(768, "karatsuba"), (768, "schoolbook"), (1024, "karatsuba")])
-def test_tma_staged_barrett_path(cuda, bits, strategy):
-    """The TMA-staged kernel (generic Barrett vmul/axpy from 24 limbs):
-    several tiles per CTA (stage reuse, both mbarrier phases), a ragged tail
-    of n mod 256 elements, an element-offset view, and out aliasing an
-    input, all against Python ints."""
+@pytest.mark.parametrize("bits,strategy,reduction", [(768, "karatsuba", "barrett"), (768, "schoolbook", "barrett"),
+                                                     (1024, "karatsuba", "barrett"), (256, "schoolbook", "auto"),
+                                                     (256, "karatsuba", "auto")])
+def test_tma_staged_path(cuda, bits, strategy, reduction):
+    """The TMA-staged kernel (generic Barrett vmul/axpy from 24 limbs, the
+    256-bit special-form axpy): several tiles per CTA (stage reuse, both
+    mbarrier phases), a ragged tail of n mod 256 elements, an element-offset
+    view, and out aliasing an input, all against Python ints."""
     import torch
     dev = _dev()
     from paper_2501_07535_b200.params import find_ntt_params
     q = find_ntt_params(bits, 1).p
-    f = dev.Field(bits, q, strategy, reduction="barrett")
+    f = dev.Field(bits, q, strategy, reduction=reduction)
     r = random.Random(bits)
     n = 256 * 700 + 77
     xs = [r.randrange(q) for _ in range(n + 1)]

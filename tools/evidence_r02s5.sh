@@ -9,7 +9,7 @@ timeout 600 python bench.py --impl reference > gpurun_out/r02s5_bench_ref.json 2
 timeout 400 python tools/stress.py 43 240 > gpurun_out/r02s5_stress_seed43.txt 2>&1
 # (compute-sanitizer is closed on this GPU pool: the TMA kernel's parity
 #  cases -- stage reuse, ragged tail, offset views, aliasing -- are in
-#  tests/test_blas_gpu.py::test_tma_staged_barrett_path and the stress run above)
+#  tests/test_blas_gpu.py::test_tma_staged_path and the stress run above)
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:blas_tma_kernel -c 1 -o gpurun_out/r02s5_tma python tools/workload.py vmul --bits 768 --reps 1 --reduction barrett --strategy karatsuba > gpurun_out/r02s5_ncu_tma.log 2>&1
 python tools/ncu_summary.py gpurun_out/r02s5_tma.ncu-rep > gpurun_out/r02s5_ncu_tma.jsonl 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r02s5_launches_bench.csv python bench.py --steps 2 --warmup 3 --skip-extras --cpu-sample 1 --python-bigint 0 > gpurun_out/r02s5_bench_under_ncu.log 2>&1
