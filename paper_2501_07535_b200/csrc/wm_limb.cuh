@@ -861,6 +861,18 @@ WM_DEV void mul_shoup_lazy_dual(uint32_t (&r1)[K], uint32_t (&r2)[K], const uint
     q1[j] = h1[K - C0 + j];
     q2[j] = h2[K - C0 + j];
   }
+#ifndef WM_SHOUP_DUAL_LO_PTX  // low halves as the single multiply forms them (PTX chains): the
+#define WM_SHOUP_DUAL_LO_PTX 1   // interleaved compiler-carry form made the pairing lose (A/B)
+#endif
+  if constexpr (WM_SHOUP_DUAL_LO_PTX) {
+    zero_n<K>(r1);
+    zero_n<K>(r2);
+    mul_lo_acc<K, kPtx>(r1, v1, w1);
+    mul_lo_acc<K, kPtx>(r2, v2, w2);
+    mul_lo_acc<K, kPtx>(r1, q1, np);
+    mul_lo_acc<K, kPtx>(r2, q2, np);
+    return;
+  }
   // low halves: r = lo(v w) + lo(qh np), compiler carries, interleaved
 #pragma unroll
   for (int j = 0; j < K; ++j) {

@@ -42,8 +42,12 @@
 // Minimum resident CTAs per SM requested from ptxas for the pass kernels
 // (caps registers at 65536 / (256 * WM_NTT_MINB)); A/B: tools/ab_timing.py.
 #ifndef WM_NTT_DUAL  // bit mask over arithmetic modes: radix-4 groups with interleaved product pairs
-#define WM_NTT_DUAL 10  // modes 3 and 1: 8.50 -> 8.34 (special form), 13.24 -> 13.08 us/transform
-                        // (BLS12-381 r); the Shoup modes 0/2 lose 2-4 % (profiles/r02_ab_ntt_dual*.txt)
+#define WM_NTT_DUAL 11  // modes 3 and 1: 8.50 -> 8.34 (special form), 13.24 -> 13.08 us/transform
+                        // (BLS12-381 r); Shoup mode 0 with the low halves as PTX chains
+                        // (WM_SHOUP_DUAL_LO_PTX): 256-bit 10.13 -> 10.00, 128-bit 3.49 -> 3.48,
+                        // but 160-224 bits 0.5-1.5 % slower, so only at 8 and <= 4 limbs
+                        // (profiles/r02_ab_shoup_dual_lo_ptx.txt); mode 2 loses 2-4 %
+                        // (profiles/r02_ab_ntt_dual*.txt)
 #endif
 #ifndef WM_PM_CANON  // special-form fields: canonicalise [0, 6p) by the top bits (A/B)
 #define WM_PM_CANON 1  // row pass 243.6 -> 238.6 us, 8.32 -> 8.25 us/transform (profiles/r02_ab_pm_canon.txt)
@@ -352,7 +356,8 @@ struct Smem {
 #endif
 template <int K, int MODE>
 __host__ __device__ constexpr bool ntt_dual() {
-  return ((WM_NTT_DUAL >> MODE) & 1) && K <= WM_NTT_DUAL_MAXK;  // (radix-2 passes start at 24 limbs)
+  return ((WM_NTT_DUAL >> MODE) & 1) && K <= WM_NTT_DUAL_MAXK &&  // (radix-2 passes start at 24 limbs)
+         (MODE != 0 || K == 8 || K <= 4);
 }
 
 // ------------------------------------------------------------------ in-smem DFT
